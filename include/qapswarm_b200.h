@@ -1,0 +1,206 @@
+/*
+ * qapswarm_b200.h -- C ABI of the B200-native multi-swarm PSO step for QAP.
+ *
+ * Drop-in boundary for the reference package `qapswarm` (arXiv 1504.05158
+ * restatement; paths below are relative to
+ * /root/reference/pkg/src/qapswarm/).  The reference binds its hot path from
+ * Python (engine.step, engine.py:196-208) to four numba kernels; this header
+ * exposes the same operations with plain pointers and sizes, no torch types.
+ *
+ * Two tiers:
+ *   1. Reference-layout, host-buffer entry points (qsb_velocity_many,
+ *      qsb_aggregate_many, qsb_cost_many_*, qsb_step_draws_host): the same
+ *      arguments, layouts and in-place semantics as _batch.velocity_many
+ *      (_batch.py:30-58), _batch.aggregate_many (_batch.py:178-183),
+ *      _batch.cost_many (_batch.py:186-197) and streams.step_draws
+ *      (streams.py:53-64).  They copy host -> device -> host internally and
+ *      are synchronous, like the numba calls they replace.
+ *   2. Device-resident entry points on a qsb_state (caller-owned device
+ *      buffers, stream-ordered, no allocation, graph-capturable) used by the
+ *      Python engine: the fused step (phases 1-4a of engine.step), the
+ *      swarm/global best reduction (engine.py:216-229), migration
+ *      (migration.py:55-86) and helpers.
+ *
+ * Every function returns QSB_OK or an error code; qsb_strerror() names it.
+ * Validation that the reference performs in Python (SolverConfig,
+ * PsoCoefficients, engine.py:186-187 depth check) stays in the Python host
+ * layer, which raises the reference's ValueError messages.
+ */
+#ifndef QAPSWARM_B200_H
+#define QAPSWARM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB_OK 0
+#define QSB_EINVAL 1        /* bad argument (size, dtype, null pointer) */
+#define QSB_EUNSUPPORTED 2  /* shape not supported by any kernel variant */
+#define QSB_ECUDA 3         /* CUDA runtime error (see qsb_last_cuda_error) */
+#define QSB_EPERM 4         /* input matrix is not a permutation matrix */
+
+/* element types */
+#define QSB_F32 1
+#define QSB_F64 2
+#define QSB_I64 3
+#define QSB_U16 4
+
+/* step phase flags (qsb_step_phases) */
+#define QSB_PHASE_VELOCITY 1
+#define QSB_PHASE_AGGREGATE 2
+#define QSB_PHASE_COST 4
+#define QSB_PHASE_PBEST 8
+#define QSB_PHASE_STORE_V 16
+
+/* S_x modes, same codes as _batch.MODE_CODES (_batch.py:19-27) */
+#define QSB_SX_GLOBAL_MAX 0
+#define QSB_SX_PICK_COLUMN 1
+#define QSB_SX_SECOND_TARGET 2
+
+/* Device-resident particle state (engine.PopulationState, engine.py:85-124),
+ * structure of arrays.  Positions are int16 permutations perm[c] = row of
+ * the 1 in column c (core.py:5-6); the 0/1 matrices are never stored. */
+typedef struct qsb_state {
+  int32_t n;                 /* problem size */
+  int32_t vstride;           /* V elements per particle (>= n*n, 16-byte multiple) */
+  int32_t v_dtype;           /* QSB_F32 (throughput) or QSB_F64 (parity) */
+  int32_t cost_dtype;        /* QSB_I64 (integral instance) or QSB_F64 */
+  int64_t num_particles;     /* particles on this device */
+  int64_t swarm_size;
+  int64_t num_swarms;        /* swarms on this device */
+  int64_t particle_offset;   /* global id of local particle 0 */
+  int64_t swarm_offset;      /* global id of local swarm 0 */
+  void* V;                   /* (P, vstride) */
+  int16_t* perm;             /* (P, n) current position X */
+  int16_t* perm_new;         /* (P, n) next position */
+  int16_t* pl_perm;          /* (P, n) personal best PL */
+  void* cost;                /* (P,) goal of perm_new after a step */
+  void* pl_cost;             /* (P,) */
+  uint8_t* improved;         /* (P,) scratch: cost < pl_cost this step */
+  int16_t* pg_perm;          /* (m, n) swarm best PG */
+  void* pg_cost;             /* (m,) */
+  int16_t* best_perm;        /* (n,) best solution seen on this device */
+  void* best_cost;           /* (1,) */
+  int64_t* best_iter;        /* (1,) iteration it first appeared */
+  int64_t* best_idx;         /* (1,) global particle id it came from */
+  int64_t* iteration;        /* (1,) completed iterations t */
+  void* swarm_min;           /* (m,) scratch */
+  int64_t* swarm_min_idx;    /* (m,) scratch */
+  uint32_t* done;            /* (1,) scratch, zero-initialised */
+} qsb_state;
+
+/* QAP instance on the device (qaplib.QapInstance, qaplib.py:28-69). */
+typedef struct qsb_instance {
+  int32_t n;
+  int32_t mat_dtype;         /* QSB_U16, QSB_I64 or QSB_F64 */
+  const void* flow;          /* (n, n) row-major */
+  const void* distance;      /* (n, n) row-major */
+} qsb_instance;
+
+/* kernels.PsoCoefficients (kernels.py:47-76) plus the run seed. */
+typedef struct qsb_coeffs {
+  double c1, c2, c3, v_max;
+  int32_t normalize;         /* sv_mode == "norm" */
+  int32_t sx_mode;           /* QSB_SX_* */
+  int32_t depth;
+  int32_t reserved;
+  uint64_t seed;             /* SolverConfig.seed wrapped to uint64 (streams.py:34) */
+} qsb_coeffs;
+
+/* One migration event (migration.migrate, migration.py:55-86). */
+typedef struct qsb_migration {
+  int32_t d;                 /* SolverConfig.migration_depth (engine.py:66-68) */
+  int32_t period;            /* run when t % period == 0; 0 = unconditional */
+  int32_t mode;              /* 0 single device, 1 plan+pack, 2 apply exchanged records */
+  int32_t reserved;
+  int64_t num_swarms_total;  /* m over all devices */
+  const int32_t* picks;      /* (rows, d): host_rng(seed, t).integers(0, S) per event */
+  int64_t picks_epoch0;      /* epoch (t / period) of picks row 0 */
+  int64_t picks_rows;
+  const void* all_pg_cost;   /* (m_total,) swarm-best costs in global order */
+  int64_t* plan;             /* (d, 4) scratch: src, dst, particle, valid */
+  int64_t* records;          /* (d, n+1) donor records for exchange, or NULL */
+  double* log;               /* (log_rows, d, 6) MigrationEvent fields, or NULL */
+  int64_t log_rows;
+  int64_t* log_count;        /* (1,) events logged */
+  int32_t* status;           /* (1,) set to 1 when picks has no row for t */
+} qsb_migration;
+
+int qsb_version(void);
+const char* qsb_strerror(int code);
+int qsb_last_cuda_error(void);
+
+/* 1 if a fused step kernel exists for (n, v_dtype, mat_dtype), else 0. */
+int qsb_supported(int32_t n, int32_t v_dtype, int32_t mat_dtype);
+
+/* Elements per particle of the padded V layout for n (16-byte rows). */
+int32_t qsb_vstride(int32_t n, int32_t v_dtype);
+
+/* ---------------------------------------------------------------- tier 2
+ * Fused step, phases selected by `flags` (QSB_PHASE_*): velocity update
+ * (_batch.py:30-58) -> aggregation (_batch.py:61-183) -> goal
+ * (_batch.py:186-197) -> personal best (engine.py:211-215).  Draws come from
+ * the in-kernel Philox stream of streams.step_draws for iteration
+ * t = *state->iteration + 1 (or t_host when state->iteration is NULL), or
+ * from `inj_draws` rows (stride inj_stride doubles; r2, r3 at columns 0, 1,
+ * aggregation draws from column agg_base) when non-NULL.  `coef` (P, 2)
+ * optionally overrides (c2*r2, c3*r3). */
+int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co,
+                    int32_t flags, const double* inj_draws, int64_t inj_stride,
+                    int32_t agg_base, const double* coef, uint64_t t_host, void* stream);
+
+/* Swarm bests (argmin over improved particles, strict <) and the global best
+ * (argmin over all, strict <), engine.py:216-229; advances *iteration. */
+int qsb_best_update(const qsb_state* st, void* stream);
+
+/* One full iteration: qsb_step_phases(all) + qsb_best_update.  The caller
+ * swaps perm/perm_new afterwards (engine.py:231-232). */
+int qsb_step(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co, void* stream);
+
+/* Migration (migration.py:55-86) on the post-swap state. */
+int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream);
+
+/* Goal of P permutations (int16, device) -> out (int64 or f64, device). */
+int qsb_cost(const int16_t* perms, int64_t P, const qsb_instance* inst, void* out, void* stream);
+
+/* streams.step_draws rows p0 .. p0+P-1 into device memory. */
+int qsb_step_draws(uint64_t seed, uint64_t t, int64_t p0, int64_t P, int32_t n, double* out,
+                   void* stream);
+
+/* Throughput-mode device initialisation (documented non-reference stream). */
+int qsb_init_population_device(const qsb_state* st, uint64_t seed, double amp, void* stream);
+
+/* int16 permutations -> 0/1 matrices X[k, i] = (perm[i] == k) (device). */
+int qsb_perm_to_matrix(const int16_t* perm, int64_t P, int32_t n, int8_t* x, void* stream);
+
+/* ---------------------------------------------------------------- tier 1
+ * Reference-layout, host-buffer, synchronous drop-ins for _batch / streams. */
+
+/* _batch.velocity_many(v, x, pl, pg, swarm_size, c1, c2r2, c3r3, v_max,
+ * normalize) (_batch.py:30-58): v (P,n,n) f64 in place; x, pl (P,n,n) int8;
+ * pg (P/swarm_size, n, n) int8; c2r2, c3r3 (P,). */
+int qsb_velocity_many(double* v, const int8_t* x, const int8_t* pl, const int8_t* pg, int64_t P,
+                      int32_t n, int64_t swarm_size, double c1, const double* c2r2,
+                      const double* c3r3, double v_max, int32_t normalize);
+
+/* _batch.aggregate_many(x, v, mode, depth, draws, out_mat, out_perm)
+ * (_batch.py:178-183): draws row p at draws + p*draws_stride. */
+int qsb_aggregate_many(const int8_t* x, const double* v, int64_t P, int32_t n, int32_t mode,
+                       int32_t depth, const double* draws, int64_t draws_stride, int8_t* out_mat,
+                       int64_t* out_perm);
+
+/* _batch.cost_many(perms, flow, distance, out) (_batch.py:186-197). */
+int qsb_cost_many_i64(const int64_t* perms, const int64_t* flow, const int64_t* distance,
+                      int64_t* out, int64_t P, int32_t n);
+int qsb_cost_many_f64(const int64_t* perms, const double* flow, const double* distance,
+                      double* out, int64_t P, int32_t n);
+
+/* streams.step_draws(seed, iteration, num_particles, n) (streams.py:53-64). */
+int qsb_step_draws_host(uint64_t seed, uint64_t t, int64_t P, int32_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QAPSWARM_B200_H */

@@ -1,0 +1,35 @@
+"""qapswarm-b200: B200-native multi-swarm PSO for the Quadratic Assignment
+Problem (arXiv 1504.05158), drop-in for the reference package's solver API.
+
+The public names mirror ``qapswarm/__init__.py``: configs, population
+state, ``init_population`` / ``step`` / ``run``, migration and statistics.
+The per-iteration work runs in hand-written sm_100a kernels (libqsb.so,
+C ABI in include/qapswarm_b200.h); there is no CPU fallback.
+"""
+
+from .config import PsoCoefficients, SolverConfig, SV_MODES, SX_MODES
+from .instance import QapInstance, parse_instance, load_instance, taillard_uniform
+from .migration import SwarmBestTable, MigrationEvent, migrate
+from .stats import IterationStats, percentile, pmf, collect, export_csv, write_solution
+from .engine import (
+    PopulationState,
+    RunResult,
+    init_population,
+    step,
+    run,
+    projected_buffer_bytes,
+    device_buffer_bytes,
+    gap,
+)
+from . import batch
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "PsoCoefficients", "SolverConfig", "SV_MODES", "SX_MODES",
+    "QapInstance", "parse_instance", "load_instance", "taillard_uniform",
+    "SwarmBestTable", "MigrationEvent", "migrate",
+    "IterationStats", "percentile", "pmf", "collect", "export_csv", "write_solution",
+    "PopulationState", "RunResult", "init_population", "step", "run",
+    "projected_buffer_bytes", "device_buffer_bytes", "gap", "batch",
+]

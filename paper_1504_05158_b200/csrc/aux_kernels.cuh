@@ -1,0 +1,357 @@
+// aux_kernels.cuh -- the small kernels around the fused step:
+//   swarm/global best reduction (engine.py:216-229), migration
+//   (migration.py:55-86), the step-draw dump (streams.py:53-64), the
+//   standalone goal evaluation (_batch.py:186-197), layout conversion for
+//   the reference-layout entry points, and the device population init.
+#pragma once
+#include <type_traits>
+#include "common.cuh"
+
+namespace qsb {
+
+// ----------------------------------------------------------- best update
+struct BestArgs {
+  int n;
+  int64_t S;            // swarm size
+  int64_t m;            // local swarms
+  int64_t p0;           // global id of local particle 0 (tie-break key)
+  const void* cost;     // (P,) of perm_new
+  const uint8_t* improved;
+  const int16_t* perm_new;
+  int16_t* pg_perm;
+  void* pg_cost;
+  // global best record
+  void* best_cost;
+  int16_t* best_perm;
+  int64_t* best_iter;
+  int64_t* best_idx;     // global particle id of the record (for multi-device merges)
+  int64_t* t_dev;        // iteration counter; t = *t_dev + 1, written back at the end
+  void* swarm_min;       // (m,) scratch: per-swarm min cost over all particles
+  int64_t* swarm_min_idx;
+  unsigned* done;        // arrival counter (zero-initialised)
+};
+
+template <typename CT>
+__device__ __forceinline__ bool lex_less(CT a, int64_t ia, CT b, int64_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+template <typename CT>
+__device__ __forceinline__ void warp_lexmin(CT& c, int64_t& i) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const CT oc = __shfl_xor_sync(FULL, c, o);
+    const int64_t oi = __shfl_xor_sync(FULL, i, o);
+    if (lex_less(oc, oi, c, i)) { c = oc; i = oi; }
+  }
+}
+
+template <typename CT>
+__device__ __forceinline__ CT ct_max() {
+  if constexpr (std::is_floating_point<CT>::value) return __longlong_as_double(0x7ff0000000000000LL);
+  else return (CT)0x7fffffffffffffffLL;
+}
+
+// One warp per swarm: argmin over improved particles (first index) replaces
+// the swarm best when strictly cheaper; argmin over all particles feeds the
+// global best, which the last-arriving block applies (strict <, first index).
+template <typename CT, int WPB>
+__global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
+  const CT* cost = reinterpret_cast<const CT*>(a.cost);
+  const int n = a.n;
+  if (k < a.m) {
+    CT bi = ct_max<CT>(), ba = ct_max<CT>();
+    int64_t ii = INT64_MAX, ia = INT64_MAX;
+    const int64_t lo = k * a.S;
+    for (int64_t q = lane; q < a.S; q += 32) {
+      const int64_t i = lo + q;
+      const CT c = cost[i];
+      if (lex_less(c, i, ba, ia)) { ba = c; ia = i; }
+      if (a.improved[i] && lex_less(c, i, bi, ii)) { bi = c; ii = i; }
+    }
+    warp_lexmin(bi, ii);
+    warp_lexmin(ba, ia);
+    CT* pgc = reinterpret_cast<CT*>(a.pg_cost);
+    if (ii != INT64_MAX && bi < pgc[k]) {
+      for (int c = lane; c < n; c += 32) a.pg_perm[k * n + c] = a.perm_new[ii * n + c];
+      if (lane == 0) pgc[k] = bi;
+    }
+    if (lane == 0) {
+      reinterpret_cast<CT*>(a.swarm_min)[k] = ba;
+      a.swarm_min_idx[k] = ia;
+    }
+  }
+  // last block applies the global best
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const volatile CT* sm = reinterpret_cast<const volatile CT*>(a.swarm_min);
+  const volatile int64_t* smi = a.swarm_min_idx;
+  CT bc = ct_max<CT>();
+  int64_t bidx = INT64_MAX;
+  for (int64_t q = threadIdx.x; q < a.m; q += blockDim.x) {
+    const CT c = sm[q];
+    const int64_t i = smi[q];
+    if (lex_less(c, i, bc, bidx)) { bc = c; bidx = i; }
+  }
+  warp_lexmin(bc, bidx);
+  __shared__ CT wc[WPB];
+  __shared__ int64_t wi[WPB];
+  if (lane == 0) { wc[threadIdx.x >> 5] = bc; wi[threadIdx.x >> 5] = bidx; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    bc = lane < WPB ? wc[lane] : ct_max<CT>();
+    bidx = lane < WPB ? wi[lane] : INT64_MAX;
+    warp_lexmin(bc, bidx);
+    const int64_t t = *a.t_dev + 1;
+    CT* gb = reinterpret_cast<CT*>(a.best_cost);
+    const bool upd = bidx != INT64_MAX && bc < *gb;
+    if (upd)
+      for (int c = lane; c < n; c += 32) a.best_perm[c] = a.perm_new[bidx * n + c];
+    __syncwarp();
+    if (lane == 0) {
+      if (upd) { *gb = bc; *a.best_iter = t; *a.best_idx = a.p0 + bidx; }
+      *a.t_dev = t;
+      *a.done = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------- migration
+struct MigArgs {
+  int n;
+  int64_t S;             // swarm size
+  int64_t m;             // total swarms (global)
+  int64_t m0;            // first swarm owned by this device
+  int64_t m_local;       // swarms owned by this device
+  int d;                 // replacements per event
+  int period;            // run only when t % period == 0 (0: unconditional)
+  const int64_t* t_dev;  // current iteration (already advanced by best_kernel)
+  const int32_t* picks;  // (rows, d) donor offsets j = rng.integers(0, S)
+  int64_t picks_e0;      // epoch of row 0 (epoch = t / period, or t if period == 0)
+  int64_t picks_rows;
+  const void* all_pg_cost;   // (m,) global swarm-best costs (== pg_cost on one device)
+  const int16_t* perm;   // local current particles (post-swap)
+  const void* cost;      // local current costs
+  int16_t* pg_perm;      // local swarm bests
+  void* pg_cost;
+  int64_t* plan;         // (d, 4): src, dst, particle, epoch-valid flag
+  int64_t* rec;          // (d, n+1) donor records (multi-device exchange), nullable
+  double* log;           // (log_rows, d, 6) migration events, nullable
+  int64_t log_rows;
+  int64_t* log_count;    // events written so far (device counter)
+  int* status;           // set to 1 if the picks table has no row for t
+  int mode;              // 0 fused (plan+apply), 1 plan+pack, 2 apply from rec
+};
+
+// Stable ascending rank of every swarm cost (np.argsort(kind="stable")),
+// then rank k donates to rank m-1-k (migration.py:81-90).
+template <typename CT>
+__global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  const int64_t t = *a.t_dev;
+  if (a.period > 0 && (t % a.period) != 0) return;
+  const int64_t epoch = a.period > 0 ? t / a.period : t;
+  const int64_t row = epoch - a.picks_e0;
+  if (a.mode != 2 && (row < 0 || row >= a.picks_rows)) {
+    if (threadIdx.x == 0) *a.status = 1;
+    return;
+  }
+  const int n = a.n;
+  const int64_t m = a.m;
+  CT* pgc = reinterpret_cast<CT*>(a.pg_cost);
+  const CT* lcost = reinterpret_cast<const CT*>(a.cost);
+  if (a.mode == 2) {
+    for (int k = threadIdx.x; k < a.d; k += blockDim.x) {
+      const int64_t dst = a.plan[4 * k + 1] - a.m0;
+      if (dst < 0 || dst >= a.m_local) continue;
+      const int64_t* r = a.rec + (int64_t)k * (n + 1);
+      CT c;
+      if constexpr (std::is_floating_point<CT>::value) c = __longlong_as_double(r[0]);
+      else c = (CT)r[0];
+      pgc[dst] = c;
+      for (int q = 0; q < n; ++q) a.pg_perm[dst * n + q] = (int16_t)r[1 + q];
+    }
+    if (a.log && a.log_count && *a.log_count >= a.d) {
+      // complete the events with the donors' costs (known only after the exchange)
+      const int64_t row0 = (*a.log_count / a.d - 1) * a.d;
+      for (int k = threadIdx.x; k < a.d; k += blockDim.x) {
+        const int64_t* r = a.rec + (int64_t)k * (n + 1);
+        double c;
+        if constexpr (std::is_floating_point<CT>::value) c = __longlong_as_double(r[0]);
+        else c = (double)r[0];
+        a.log[(row0 + k) * 6 + 5] = c;
+      }
+    }
+    return;
+  }
+  CT* sc = reinterpret_cast<CT*>(msm);
+  int32_t* order = reinterpret_cast<int32_t*>(msm + align_up(m * sizeof(CT), 16));
+  const CT* allc = reinterpret_cast<const CT*>(a.all_pg_cost);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) sc[i] = allc[i];
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const CT ci = sc[i];
+    int64_t r = 0;
+    for (int64_t j = 0; j < m; ++j) {
+      const CT cj = sc[j];
+      r += (cj < ci) || (cj == ci && j < i);
+    }
+    order[r] = (int32_t)i;
+  }
+  __syncthreads();
+  const int32_t* picks = a.picks + row * a.d;
+  for (int k = threadIdx.x; k < a.d; k += blockDim.x) {
+    const int64_t src = order[k];
+    const int64_t dst = order[m - 1 - k];
+    const int64_t particle = src * a.S + picks[k];
+    const int64_t lp = particle - a.m0 * a.S;
+    const bool src_local = src >= a.m0 && src < a.m0 + a.m_local;
+    const bool dst_local = dst >= a.m0 && dst < a.m0 + a.m_local;
+    a.plan[4 * k + 0] = src;
+    a.plan[4 * k + 1] = dst;
+    a.plan[4 * k + 2] = particle;
+    a.plan[4 * k + 3] = 1;
+    if (a.log && (*a.log_count / a.d) < a.log_rows) {
+      double* e = a.log + ((*a.log_count / a.d) * a.d + k) * 6;
+      e[0] = (double)t; e[1] = (double)src; e[2] = (double)dst; e[3] = (double)particle;
+      e[4] = (double)sc[dst];
+      e[5] = src_local ? (double)lcost[lp] : 0.0;   // multi-device: filled by the host
+    }
+    if (a.mode == 0) {
+      // one device owns everything: donor read + swarm-best write in place
+      pgc[dst] = lcost[lp];
+      for (int q = 0; q < n; ++q) a.pg_perm[dst * n + q] = a.perm[lp * n + q];
+    } else if (a.rec) {
+      int64_t* r = a.rec + (int64_t)k * (n + 1);
+      if (src_local) {
+        if constexpr (std::is_floating_point<CT>::value) r[0] = __double_as_longlong(lcost[lp]);
+        else r[0] = (int64_t)lcost[lp];
+        for (int q = 0; q < n; ++q) r[1 + q] = a.perm[lp * n + q];
+      } else {
+        for (int q = 0; q <= n; ++q) r[q] = 0;
+      }
+    }
+    (void)dst_local;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && a.log && (*a.log_count / a.d) < a.log_rows) *a.log_count += a.d;
+}
+
+// --------------------------------------------------------- draws (debug)
+__global__ void draws_kernel(uint64_t seed, uint64_t t, int64_t p0, int64_t P, int n, double* out) {
+  const int64_t w = 2 + 2 * (int64_t)n;
+  const int64_t total = P * w;
+  const uint64_t word1 = stream_word(2, t);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = (uint64_t)(p0 * w + e);
+    const PhiloxBlock b = philox4x64_10((idx >> 2) + 1, seed, word1);
+    out[e] = u64_to_unit(b.v[idx & 3]);
+  }
+}
+
+// ------------------------------------------------------ standalone goal
+template <typename MT, typename PT>
+__global__ void cost_kernel(const PT* perms, int64_t P, int n, const MT* F, const MT* D, void* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += nw) {
+    const PT* pp = perms + p * n;
+    if constexpr (std::is_floating_point<MT>::value) {
+      if (lane == 0) {
+        double acc = (double)F[0] * (double)D[0] * 0.0;
+        for (int i = 0; i < n; ++i) {
+          const int64_t pi = pp[i];
+          for (int j = 0; j < n; ++j)
+            acc = __dadd_rn(acc, __dmul_rn((double)F[i * n + j], (double)D[pi * n + pp[j]]));
+        }
+        reinterpret_cast<double*>(out)[p] = acc;
+      }
+    } else {
+      uint64_t part = 0;
+      for (int j = lane; j < n; j += 32) {
+        const int64_t pj = pp[j];
+        for (int i = 0; i < n; ++i) part += (uint64_t)F[i * n + j] * (uint64_t)D[(int64_t)pp[i] * n + pj];
+      }
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+      if (lane == 0) reinterpret_cast<int64_t*>(out)[p] = (int64_t)part;
+    }
+  }
+}
+
+// ------------------------------------------------------- layout helpers
+// Reference layout X[k, i] = 1 iff k == perm[i] (core.py:5-6) -> perm.
+// bad[0] is set when a column does not hold exactly one 1.
+__global__ void mat_to_perm_kernel(const int8_t* x, int64_t P, int n, int16_t* perm, int* bad) {
+  const int64_t total = P * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / n;
+    const int c = (int)(e % n);
+    const int8_t* xp = x + p * n * n;
+    int r1 = -1, ones = 0;
+    for (int r = 0; r < n; ++r) if (xp[r * n + c] == 1) { ++ones; r1 = r; }
+    if (ones != 1) { atomicExch(bad, 1); r1 = 0; }
+    perm[e] = (int16_t)r1;
+  }
+}
+
+template <typename PT>
+__global__ void perm_to_mat_kernel(const PT* perm, int64_t P, int n, int8_t* x) {
+  const int64_t total = P * n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / ((int64_t)n * n);
+    const int rc = (int)(e % ((int64_t)n * n));
+    const int r = rc / n, c = rc % n;
+    x[e] = (perm[p * n + c] == r) ? 1 : 0;
+  }
+}
+
+// -------------------------------------------- device population init
+// Throughput-mode initialisation (NOT the reference's init stream): every
+// particle draws a Fisher-Yates permutation and U(-amp, amp) velocities from
+// Philox keyed (seed, 4<<56); particle rows are counter offsets, so the
+// result is independent of the device count.
+template <typename VT>
+__global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vstride, double amp,
+                            int16_t* perm, VT* V) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t word1 = stream_word(4, 0);
+  const int64_t nn = (int64_t)n * n;
+  const uint64_t row_w = (uint64_t)(nn + n);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += nw) {
+    const uint64_t base = (uint64_t)(p0 + p) * row_w;
+    VT* vp = V + p * vstride;
+    for (int64_t e = lane; e < vstride; e += 32) {
+      if (e < nn) {
+        const uint64_t idx = base + (uint64_t)e;
+        const double u = u64_to_unit(philox4x64_10((idx >> 2) + 1, seed, word1).v[idx & 3]);
+        vp[e] = (VT)(-amp + 2.0 * amp * u);
+      } else {
+        vp[e] = (VT)0;
+      }
+    }
+    if (lane == 0) {
+      int16_t* pp = perm + p * n;
+      for (int i = 0; i < n; ++i) pp[i] = (int16_t)i;
+      DrawRow dr; dr.inj = nullptr; dr.seed = seed; dr.word1 = word1;
+      dr.base = base + (uint64_t)nn; dr.cached = ~0ULL;
+      for (int i = n - 1; i > 0; --i) {
+        long long j = (long long)(dr.at(n - 1 - i) * (double)(i + 1));
+        if (j > i) j = i;
+        const int16_t tmp = pp[i]; pp[i] = pp[j]; pp[j] = tmp;
+      }
+    }
+  }
+}
+
+}  // namespace qsb

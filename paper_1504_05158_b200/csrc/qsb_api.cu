@@ -1,0 +1,536 @@
+// qsb_api.cu -- extern "C" entry points of libqsb (include/qapswarm_b200.h).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/qapswarm_b200.h"
+#include "aux_kernels.cuh"
+#include "step_kernel.cuh"
+
+using namespace qsb;
+
+static thread_local int g_last_cuda = 0;
+
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return QSB_OK;
+  g_last_cuda = (int)e;
+  return QSB_ECUDA;
+}
+
+static int launch_status() { return cuda_status(cudaGetLastError()); }
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static size_t smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (v <= 0) v = 227 * 1024;
+  }
+  return (size_t)v;
+}
+
+// ------------------------------------------------------------ fused step
+template <typename VT, typename MT, int G, int CPL, int W>
+static int launch_step(const StepArgs& a, cudaStream_t s) {
+  using K = StepKernel<VT, MT, G, CPL, W>;
+  StepArgs b = a;
+  const bool need_fd = (a.flags & F_COST) != 0;
+  b.fd_smem = need_fd && (G == 1 || K::smem_bytes(a.n, a.vstride, true) <= smem_optin());
+  const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
+  if (smem > smem_optin()) return QSB_EUNSUPPORTED;
+  auto fn = step_kernel<VT, MT, G, CPL, W>;
+  static size_t attr_smem = 0;
+  static size_t occ_smem = 0;
+  static int occ_blocks = 0;
+  if (smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr_smem = smem;
+  }
+  if (occ_smem != smem) {
+    int bps = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 32 * G * W, smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    occ_blocks = bps > 0 ? bps : 1;
+    occ_smem = smem;
+  }
+  if (a.P <= 0) return QSB_OK;
+  const int64_t want = (a.P + W - 1) / W;
+  const int64_t cap = (int64_t)num_sms() * occ_blocks;
+  const int grid = (int)(want < cap ? want : cap);
+  fn<<<grid, 32 * G * W, smem, s>>>(b);
+  return launch_status();
+}
+
+template <typename VT, typename MT, bool DRY>
+static int dispatch_n(const StepArgs& a, cudaStream_t s) {
+  if (a.n <= 32) {
+    if constexpr (DRY) return StepKernel<VT, MT, 1, 1, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
+    else return launch_step<VT, MT, 1, 1, 4>(a, s);
+  }
+  if (a.n <= 64) {
+    if constexpr (DRY) return StepKernel<VT, MT, 1, 2, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
+    else return launch_step<VT, MT, 1, 2, 4>(a, s);
+  }
+  if (a.n <= 128) {
+    if constexpr (DRY) return StepKernel<VT, MT, 4, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
+    else return launch_step<VT, MT, 4, 1, 1>(a, s);
+  }
+  if (a.n <= 256) {
+    if constexpr (DRY) return StepKernel<VT, MT, 8, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
+    else return launch_step<VT, MT, 8, 1, 1>(a, s);
+  }
+  return QSB_EUNSUPPORTED;
+}
+
+template <bool DRY>
+static int dispatch(int v_dtype, int mat_dtype, const StepArgs& a, cudaStream_t s) {
+  if (v_dtype == QSB_F32) {
+    if (mat_dtype == QSB_U16) return dispatch_n<float, uint16_t, DRY>(a, s);
+    if (mat_dtype == QSB_I64) return dispatch_n<float, int64_t, DRY>(a, s);
+    if (mat_dtype == QSB_F64) return dispatch_n<float, double, DRY>(a, s);
+  } else if (v_dtype == QSB_F64) {
+    if (mat_dtype == QSB_U16) return dispatch_n<double, uint16_t, DRY>(a, s);
+    if (mat_dtype == QSB_I64) return dispatch_n<double, int64_t, DRY>(a, s);
+    if (mat_dtype == QSB_F64) return dispatch_n<double, double, DRY>(a, s);
+  }
+  return QSB_EINVAL;
+}
+
+static int32_t vstride_of(int32_t n, int32_t v_dtype) {
+  const int32_t per16 = v_dtype == QSB_F64 ? 2 : 4;
+  const int32_t nn = n * n;
+  return (nn + per16 - 1) / per16 * per16;
+}
+
+extern "C" {
+
+int qsb_version(void) { return 10000; }
+
+const char* qsb_strerror(int code) {
+  switch (code) {
+    case QSB_OK: return "ok";
+    case QSB_EINVAL: return "invalid argument";
+    case QSB_EUNSUPPORTED: return "problem size not supported by the fused kernel";
+    case QSB_ECUDA: return cudaGetErrorString((cudaError_t)g_last_cuda);
+    case QSB_EPERM: return "input is not a permutation matrix";
+    default: return "unknown error";
+  }
+}
+
+int qsb_last_cuda_error(void) { return g_last_cuda; }
+
+int32_t qsb_vstride(int32_t n, int32_t v_dtype) { return vstride_of(n, v_dtype); }
+
+int qsb_supported(int32_t n, int32_t v_dtype, int32_t mat_dtype) {
+  if (n < 2) return 0;
+  StepArgs a{};
+  a.n = n;
+  a.vstride = vstride_of(n, v_dtype);
+  return dispatch<true>(v_dtype, mat_dtype, a, nullptr) == QSB_OK ? 1 : 0;
+}
+
+static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co) {
+  a.n = st->n;
+  a.vstride = st->vstride;
+  a.P = st->num_particles;
+  a.S = st->swarm_size;
+  a.p0 = st->particle_offset;
+  a.c1 = co->c1; a.c2 = co->c2; a.c3 = co->c3; a.vmax = co->v_max;
+  a.normalize = co->normalize;
+  a.mode = co->sx_mode;
+  a.depth = co->depth;
+  a.seed = co->seed;
+  a.V = st->V;
+  a.perm = st->perm;
+  a.perm_new = st->perm_new;
+  a.pl_perm = st->pl_perm;
+  a.pg_perm = st->pg_perm;
+  a.cost = st->cost;
+  a.pl_cost = st->pl_cost;
+  a.improved = st->improved;
+  a.F = inst ? inst->flow : nullptr;
+  a.D = inst ? inst->distance : nullptr;
+}
+
+int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co,
+                    int32_t flags, const double* inj_draws, int64_t inj_stride, int32_t agg_base,
+                    const double* coef, uint64_t t_host, void* stream) {
+  if (!st || !co || st->n < 2 || st->vstride < st->n * st->n) return QSB_EINVAL;
+  if ((flags & (QSB_PHASE_COST | QSB_PHASE_PBEST)) && !(flags & QSB_PHASE_AGGREGATE)) return QSB_EINVAL;
+  if ((flags & QSB_PHASE_COST) && (!inst || inst->n != st->n)) return QSB_EINVAL;
+  if (co->sx_mode < 0 || co->sx_mode > 2) return QSB_EINVAL;
+  StepArgs a{};
+  fill_args(a, st, inst, co);
+  a.flags = flags;
+  a.t_dev = st->iteration;
+  a.t_host = t_host;
+  a.inj_draws = inj_draws;
+  a.inj_stride = inj_stride;
+  a.agg_base = agg_base;
+  a.coef = coef;
+  const int mat = inst ? inst->mat_dtype : QSB_U16;
+  return dispatch<false>(st->v_dtype, mat, a, (cudaStream_t)stream);
+}
+
+int qsb_best_update(const qsb_state* st, void* stream) {
+  if (!st || !st->iteration || !st->done) return QSB_EINVAL;
+  BestArgs b{};
+  b.n = st->n;
+  b.S = st->swarm_size;
+  b.m = st->num_swarms;
+  b.p0 = st->particle_offset;
+  b.cost = st->cost;
+  b.improved = st->improved;
+  b.perm_new = st->perm_new;
+  b.pg_perm = st->pg_perm;
+  b.pg_cost = st->pg_cost;
+  b.best_cost = st->best_cost;
+  b.best_perm = st->best_perm;
+  b.best_iter = st->best_iter;
+  b.best_idx = st->best_idx;
+  b.t_dev = st->iteration;
+  b.swarm_min = st->swarm_min;
+  b.swarm_min_idx = st->swarm_min_idx;
+  b.done = st->done;
+  constexpr int WPB = 8;
+  const int grid = (int)((b.m + WPB - 1) / WPB);
+  if (grid <= 0) return QSB_EINVAL;
+  if (st->cost_dtype == QSB_I64)
+    best_kernel<int64_t, WPB><<<grid, 32 * WPB, 0, (cudaStream_t)stream>>>(b);
+  else if (st->cost_dtype == QSB_F64)
+    best_kernel<double, WPB><<<grid, 32 * WPB, 0, (cudaStream_t)stream>>>(b);
+  else
+    return QSB_EINVAL;
+  return launch_status();
+}
+
+int qsb_step(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co, void* stream) {
+  int rc = qsb_step_phases(st, inst, co,
+                           QSB_PHASE_VELOCITY | QSB_PHASE_AGGREGATE | QSB_PHASE_COST |
+                               QSB_PHASE_PBEST | QSB_PHASE_STORE_V,
+                           nullptr, 0, 2, nullptr, 0, stream);
+  if (rc) return rc;
+  return qsb_best_update(st, stream);
+}
+
+int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
+  if (!st || !mig || !st->iteration || mig->d < 0) return QSB_EINVAL;
+  if (mig->d == 0) return QSB_OK;
+  if (2 * (int64_t)mig->d >= mig->num_swarms_total) return QSB_EINVAL;
+  MigArgs a{};
+  a.n = st->n;
+  a.S = st->swarm_size;
+  a.m = mig->num_swarms_total;
+  a.m0 = st->swarm_offset;
+  a.m_local = st->num_swarms;
+  a.d = mig->d;
+  a.period = mig->period;
+  a.t_dev = st->iteration;
+  a.picks = mig->picks;
+  a.picks_e0 = mig->picks_epoch0;
+  a.picks_rows = mig->picks_rows;
+  a.all_pg_cost = mig->all_pg_cost ? mig->all_pg_cost : st->pg_cost;
+  a.perm = st->perm;
+  a.cost = st->cost;
+  a.pg_perm = st->pg_perm;
+  a.pg_cost = st->pg_cost;
+  a.plan = mig->plan;
+  a.rec = mig->records;
+  a.log = mig->log;
+  a.log_rows = mig->log_rows;
+  a.log_count = mig->log_count;
+  a.status = mig->status;
+  a.mode = mig->mode;
+  if (!a.plan || !a.status || (a.log && !a.log_count)) return QSB_EINVAL;
+  if (a.mode == 0 && (a.m0 != 0 || a.m_local != a.m)) return QSB_EINVAL;
+  if (a.mode == 2 && !a.rec) return QSB_EINVAL;
+  const size_t csz = st->cost_dtype == QSB_F64 ? 8 : 8;
+  const size_t smem = align_up((size_t)a.m * csz, 16) + (size_t)a.m * 4;
+  if (smem > smem_optin()) return QSB_EUNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (st->cost_dtype == QSB_I64) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(migrate_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    migrate_kernel<int64_t><<<1, 1024, smem, s>>>(a);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(migrate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    migrate_kernel<double><<<1, 1024, smem, s>>>(a);
+  }
+  return launch_status();
+}
+
+int qsb_cost(const int16_t* perms, int64_t P, const qsb_instance* inst, void* out, void* stream) {
+  if (!perms || !inst || !out || P < 0 || inst->n < 2) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  const int grid = (int)((P + 7) / 8 < 4 * num_sms() ? (P + 7) / 8 : 4 * num_sms());
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (inst->mat_dtype) {
+    case QSB_U16:
+      cost_kernel<uint16_t, int16_t><<<grid, 256, 0, s>>>(perms, P, inst->n, (const uint16_t*)inst->flow,
+                                                         (const uint16_t*)inst->distance, out);
+      break;
+    case QSB_I64:
+      cost_kernel<int64_t, int16_t><<<grid, 256, 0, s>>>(perms, P, inst->n, (const int64_t*)inst->flow,
+                                                        (const int64_t*)inst->distance, out);
+      break;
+    case QSB_F64:
+      cost_kernel<double, int16_t><<<grid, 256, 0, s>>>(perms, P, inst->n, (const double*)inst->flow,
+                                                       (const double*)inst->distance, out);
+      break;
+    default:
+      return QSB_EINVAL;
+  }
+  return launch_status();
+}
+
+int qsb_step_draws(uint64_t seed, uint64_t t, int64_t p0, int64_t P, int32_t n, double* out, void* stream) {
+  if (!out || P < 0 || n < 1) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  const int64_t total = P * (2 + 2 * (int64_t)n);
+  const int grid = (int)((total + 255) / 256 < 8 * num_sms() ? (total + 255) / 256 : 8 * num_sms());
+  draws_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, t, p0, P, n, out);
+  return launch_status();
+}
+
+int qsb_init_population_device(const qsb_state* st, uint64_t seed, double amp, void* stream) {
+  if (!st || !st->perm || !st->V) return QSB_EINVAL;
+  const int grid = (int)((st->num_particles + 7) / 8 < 8 * num_sms() ? (st->num_particles + 7) / 8 : 8 * num_sms());
+  if (grid <= 0) return QSB_OK;
+  if (st->v_dtype == QSB_F32)
+    init_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, st->particle_offset, st->num_particles,
+                                                                st->n, st->vstride, amp, st->perm, (float*)st->V);
+  else
+    init_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, st->particle_offset, st->num_particles,
+                                                                 st->n, st->vstride, amp, st->perm, (double*)st->V);
+  return launch_status();
+}
+
+int qsb_perm_to_matrix(const int16_t* perm, int64_t P, int32_t n, int8_t* x, void* stream) {
+  if (!perm || !x || P < 0 || n < 1) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  const int64_t total = P * n * n;
+  const int grid = (int)((total + 255) / 256 < 8 * num_sms() ? (total + 255) / 256 : 8 * num_sms());
+  perm_to_mat_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(perm, P, n, x);
+  return launch_status();
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- tier 1: host buffers
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return QSB_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+    if (e != cudaSuccess) return cuda_status(e);
+    cap = bytes;
+    return QSB_OK;
+  }
+};
+
+struct HostCtx {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  DevBuf b[10];
+  int init() {
+    if (!stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
+    return QSB_OK;
+  }
+};
+
+HostCtx& hctx() {
+  static HostCtx c;
+  return c;
+}
+
+#define QSB_TRY(x) do { int _rc = (x); if (_rc) return _rc; } while (0)
+#define QSB_CUDA(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return cuda_status(_e); } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int qsb_velocity_many(double* v, const int8_t* x, const int8_t* pl, const int8_t* pg, int64_t P, int32_t n,
+                      int64_t swarm_size, double c1, const double* c2r2, const double* c3r3, double v_max,
+                      int32_t normalize) {
+  if (!v || !x || !pl || !pg || !c2r2 || !c3r3 || n < 1 || P < 0 || swarm_size < 1) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  if (n < 2) return QSB_EUNSUPPORTED;
+  HostCtx& h = hctx();
+  std::lock_guard<std::mutex> lock(h.mu);
+  QSB_TRY(h.init());
+  const int64_t nn = (int64_t)n * n;
+  const int64_t m = (P + swarm_size - 1) / swarm_size;
+  const int32_t vs = vstride_of(n, QSB_F64);
+  cudaStream_t s = h.stream;
+  QSB_TRY(h.b[0].ensure(P * vs * 8));
+  QSB_TRY(h.b[1].ensure((P * 2 + m) * nn));
+  QSB_TRY(h.b[2].ensure((P * 2 + m) * n * 2));
+  QSB_TRY(h.b[3].ensure(P * 16));
+  QSB_TRY(h.b[4].ensure(16));
+  double* dV = (double*)h.b[0].p;
+  int8_t* dx = (int8_t*)h.b[1].p;
+  int8_t* dpl = dx + P * nn;
+  int8_t* dpg = dpl + P * nn;
+  int16_t* pp = (int16_t*)h.b[2].p;
+  int16_t* ppl = pp + P * n;
+  int16_t* ppg = ppl + P * n;
+  double* dcoef = (double*)h.b[3].p;
+  int* bad = (int*)h.b[4].p;
+  QSB_CUDA(cudaMemcpy2DAsync(dV, vs * 8, v, nn * 8, nn * 8, P, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dx, x, P * nn, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dpl, pl, P * nn, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dpg, pg, m * nn, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpy2DAsync(dcoef, 16, c2r2, 8, 8, P, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpy2DAsync(dcoef + 1, 16, c3r3, 8, 8, P, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+  const int grid = 4 * num_sms();
+  mat_to_perm_kernel<<<grid, 256, 0, s>>>(dx, 2 * P + m, n, pp, bad);
+  QSB_TRY(launch_status());
+  int hbad = 0;
+  QSB_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  if (hbad) return QSB_EPERM;
+  qsb_state st{};
+  st.n = n; st.vstride = vs; st.v_dtype = QSB_F64; st.cost_dtype = QSB_I64;
+  st.num_particles = P; st.swarm_size = swarm_size; st.num_swarms = m;
+  st.V = dV; st.perm = pp; st.pl_perm = ppl; st.pg_perm = ppg;
+  qsb_coeffs co{};
+  co.c1 = c1; co.v_max = v_max; co.normalize = normalize; co.sx_mode = 0; co.depth = 1;
+  QSB_TRY(qsb_step_phases(&st, nullptr, &co, QSB_PHASE_VELOCITY | QSB_PHASE_STORE_V, nullptr, 0, 2, dcoef, 1, s));
+  QSB_CUDA(cudaMemcpy2DAsync(v, nn * 8, dV, vs * 8, nn * 8, P, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  return QSB_OK;
+}
+
+int qsb_aggregate_many(const int8_t* x, const double* v, int64_t P, int32_t n, int32_t mode, int32_t depth,
+                       const double* draws, int64_t draws_stride, int8_t* out_mat, int64_t* out_perm) {
+  if (!x || !v || !draws || !out_mat || !out_perm || n < 1 || P < 0 || mode < 0 || mode > 2) return QSB_EINVAL;
+  if (draws_stride < 2 * (int64_t)n) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  if (n < 2) return QSB_EUNSUPPORTED;
+  HostCtx& h = hctx();
+  std::lock_guard<std::mutex> lock(h.mu);
+  QSB_TRY(h.init());
+  const int64_t nn = (int64_t)n * n;
+  const int32_t vs = vstride_of(n, QSB_F64);
+  cudaStream_t s = h.stream;
+  QSB_TRY(h.b[0].ensure(P * vs * 8));
+  QSB_TRY(h.b[1].ensure(P * nn));
+  QSB_TRY(h.b[2].ensure(P * n * 2 * 2));
+  QSB_TRY(h.b[3].ensure(P * draws_stride * 8));
+  QSB_TRY(h.b[4].ensure(16));
+  QSB_TRY(h.b[5].ensure(P * nn));
+  double* dV = (double*)h.b[0].p;
+  int8_t* dx = (int8_t*)h.b[1].p;
+  int16_t* pp = (int16_t*)h.b[2].p;
+  int16_t* pnew = pp + P * n;
+  double* dd = (double*)h.b[3].p;
+  int* bad = (int*)h.b[4].p;
+  int8_t* dmat = (int8_t*)h.b[5].p;
+  QSB_CUDA(cudaMemcpy2DAsync(dV, vs * 8, v, nn * 8, nn * 8, P, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dx, x, P * nn, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dd, draws, P * draws_stride * 8, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+  mat_to_perm_kernel<<<4 * num_sms(), 256, 0, s>>>(dx, P, n, pp, bad);
+  QSB_TRY(launch_status());
+  int hbad = 0;
+  QSB_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  if (hbad) return QSB_EPERM;
+  qsb_state st{};
+  st.n = n; st.vstride = vs; st.v_dtype = QSB_F64; st.cost_dtype = QSB_I64;
+  st.num_particles = P; st.swarm_size = P; st.num_swarms = 1;
+  st.V = dV; st.perm = pp; st.perm_new = pnew;
+  qsb_coeffs co{};
+  co.sx_mode = mode; co.depth = depth;
+  QSB_TRY(qsb_step_phases(&st, nullptr, &co, QSB_PHASE_AGGREGATE, dd, draws_stride, 0, nullptr, 1, s));
+  QSB_TRY(qsb_perm_to_matrix(pnew, P, n, dmat, s));
+  std::vector<int16_t> hp((size_t)(P * n));
+  QSB_CUDA(cudaMemcpyAsync(hp.data(), pnew, P * n * 2, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaMemcpyAsync(out_mat, dmat, P * nn, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < P * n; ++i) out_perm[i] = hp[(size_t)i];
+  return QSB_OK;
+}
+
+static int cost_many_host(const int64_t* perms, const void* flow, const void* dist, void* out, int64_t P,
+                          int32_t n, int mat_dtype) {
+  if (!perms || !flow || !dist || !out || n < 1 || P < 0) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  HostCtx& h = hctx();
+  std::lock_guard<std::mutex> lock(h.mu);
+  QSB_TRY(h.init());
+  const int64_t nn = (int64_t)n * n;
+  cudaStream_t s = h.stream;
+  QSB_TRY(h.b[6].ensure(P * n * 8));
+  QSB_TRY(h.b[7].ensure(2 * nn * 8));
+  QSB_TRY(h.b[8].ensure(P * 8));
+  int64_t* dp = (int64_t*)h.b[6].p;
+  char* dm = (char*)h.b[7].p;
+  QSB_CUDA(cudaMemcpyAsync(dp, perms, P * n * 8, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dm, flow, nn * 8, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dm + nn * 8, dist, nn * 8, cudaMemcpyHostToDevice, s));
+  const int grid = (int)((P + 7) / 8 < 4 * num_sms() ? (P + 7) / 8 : 4 * num_sms());
+  if (mat_dtype == QSB_I64)
+    cost_kernel<int64_t, int64_t><<<grid, 256, 0, s>>>(dp, P, n, (const int64_t*)dm,
+                                                      (const int64_t*)(dm + nn * 8), h.b[8].p);
+  else
+    cost_kernel<double, int64_t><<<grid, 256, 0, s>>>(dp, P, n, (const double*)dm,
+                                                     (const double*)(dm + nn * 8), h.b[8].p);
+  QSB_TRY(launch_status());
+  QSB_CUDA(cudaMemcpyAsync(out, h.b[8].p, P * 8, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  return QSB_OK;
+}
+
+int qsb_cost_many_i64(const int64_t* perms, const int64_t* flow, const int64_t* distance, int64_t* out,
+                      int64_t P, int32_t n) {
+  return cost_many_host(perms, flow, distance, out, P, n, QSB_I64);
+}
+
+int qsb_cost_many_f64(const int64_t* perms, const double* flow, const double* distance, double* out,
+                      int64_t P, int32_t n) {
+  return cost_many_host(perms, flow, distance, out, P, n, QSB_F64);
+}
+
+int qsb_step_draws_host(uint64_t seed, uint64_t t, int64_t P, int32_t n, double* out) {
+  if (!out || P < 0 || n < 1) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  HostCtx& h = hctx();
+  std::lock_guard<std::mutex> lock(h.mu);
+  QSB_TRY(h.init());
+  const int64_t bytes = P * (2 + 2 * (int64_t)n) * 8;
+  QSB_TRY(h.b[9].ensure(bytes));
+  QSB_TRY(qsb_step_draws(seed, t, 0, P, n, (double*)h.b[9].p, h.stream));
+  QSB_CUDA(cudaMemcpyAsync(out, h.b[9].p, bytes, cudaMemcpyDeviceToHost, h.stream));
+  QSB_CUDA(cudaStreamSynchronize(h.stream));
+  return QSB_OK;
+}
+
+}  // extern "C"

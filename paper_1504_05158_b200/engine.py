@@ -1,0 +1,483 @@
+"""The B200 solver engine: device-resident population, the fused step, runs.
+
+Mirrors the reference engine (engine.py:29-307) -- same public functions,
+signatures, field names and error messages -- while the particle state
+lives in HBM as structure-of-arrays torch tensors and every phase of an
+iteration runs in the sm_100a kernels of libqsb.so:
+
+    reference phase (engine.step)          here
+    -------------------------------------  ------------------------------------
+    streams.step_draws   (engine.py:189)   in-kernel Philox, zero HBM bytes
+    velocity_many        (engine.py:197)   \
+    aggregate_many       (engine.py:203)    > one fused kernel (qsb_step)
+    cost_many            (engine.py:207)    |
+    personal bests       (engine.py:211)   /
+    swarm/global bests   (engine.py:216)   best_kernel (one launch)
+    X <-> X_new swap     (engine.py:231)   pointer swap of perm / perm_new
+    migrate              (engine.py:235)   migrate_kernel (+ host picks)
+
+Positions are int16 permutations (perm[c] = row of the 1 in column c,
+core.py:5-6); the reference's 0/1 matrices, float64 velocities and int64
+permutations are materialised on demand by the host-view properties of
+:class:`PopulationState` (``X``, ``V``, ``PL``, ``perms``, ``bests`` ...).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import SX_CODES, PsoCoefficients, SolverConfig
+from .instance import device_format, is_integral
+from .migration import MigrationEvent, SwarmBestTable
+from .stats import IterationStats, collect
+
+PHASE_INIT, PHASE_STEP, PHASE_HOST = 1, 2, 3
+_ITER_LIMIT = 1 << 32
+_PARTICLE_LIMIT = 1 << 24
+_LOG_EPOCHS = 256
+
+
+def phase_rng(seed: int, phase: int, iteration: int) -> np.random.Generator:
+    """numpy Philox keyed (seed, phase << 56 | iteration << 24) -- the
+    reference's stream contract (streams.py:30-40)."""
+    if not 0 <= iteration < _ITER_LIMIT:
+        raise ValueError(f"iteration {iteration} outside supported range")
+    key = np.array([int(seed) & (2**64 - 1), (phase << 56) | (iteration << 24)], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def projected_buffer_bytes(config: SolverConfig, n: int) -> int:
+    """The reference's host-buffer estimate (engine.py:71-82), kept for
+    drop-in memory guards."""
+    p = config.num_particles
+    mats = 3 * p * n * n * 1 + p * n * n * 8
+    perms = 3 * p * n * 8
+    tables = 3 * p * 8
+    swarm = config.swarms * (n * n + n * 8 + 8)
+    return mats + perms + tables + swarm
+
+
+def device_buffer_bytes(config: SolverConfig, n: int) -> int:
+    """HBM bytes of this engine's state for one device holding every particle."""
+    p = config.num_particles
+    sv = 8 if config.precision == "fp64" else 4
+    vstride = -(-n * n // (16 // sv)) * (16 // sv)
+    return p * (vstride * sv + 3 * n * 2 + 2 * 8 + 1) + config.swarms * (n * 2 + 3 * 8)
+
+
+def _dev(device):
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise RuntimeError("the qapswarm-b200 engine runs on CUDA devices only")
+    return device
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else t.data_ptr()
+
+
+class PopulationState:
+    """Device-resident population (the reference's flat buffers,
+    engine.py:85-124, as int16 permutations plus the velocity tensor).
+
+    ``swarm_range`` selects the swarms this device owns (multi-GPU
+    sharding); particle ids and random streams stay global, so any split
+    reproduces the single-device trajectory.
+    """
+
+    def __init__(self, config: SolverConfig, instance, device=None, swarm_range=None):
+        n = int(instance.n)
+        dev = _dev(device)
+        m_total = config.swarms
+        m0, m1 = swarm_range if swarm_range is not None else (0, m_total)
+        if not 0 <= m0 < m1 <= m_total:
+            raise ValueError("swarm_range must be a non-empty sub-range of the swarms")
+        if m_total * config.swarm_size >= _PARTICLE_LIMIT:
+            raise ValueError(f"population {m_total * config.swarm_size} exceeds supported size")
+        S = config.swarm_size
+        p = (m1 - m0) * S
+        self.n = n
+        self.device = dev
+        self.swarms = m_total
+        self.swarm_size = S
+        self.num_particles = m_total * S
+        self.local_swarms = m1 - m0
+        self.local_particles = p
+        self.swarm_offset = m0
+        self.particle_offset = m0 * S
+        self.precision = config.precision
+        self.v_code = _lib.F64 if config.precision == "fp64" else _lib.F32
+        self.vstride = int(_lib.lib().qsb_vstride(n, self.v_code))
+        self.integral = is_integral(instance)
+        self.cost_code = _lib.I64 if self.integral else _lib.F64
+        vdt = torch.float64 if self.v_code == _lib.F64 else torch.float32
+        cdt = torch.int64 if self.integral else torch.float64
+        z = dict(device=dev)
+        try:
+            self.d_V = torch.zeros((p, self.vstride), dtype=vdt, **z)
+            self.d_perm = torch.zeros((p, n), dtype=torch.int16, **z)
+            self.d_perm_new = torch.zeros((p, n), dtype=torch.int16, **z)
+            self.d_pl_perm = torch.zeros((p, n), dtype=torch.int16, **z)
+            self.d_cost = torch.zeros(p, dtype=cdt, **z)
+            self.d_pl_cost = torch.zeros(p, dtype=cdt, **z)
+            self.d_improved = torch.zeros(p, dtype=torch.uint8, **z)
+            self.d_pg_perm = torch.zeros((self.local_swarms, n), dtype=torch.int16, **z)
+            self.d_pg_cost = torch.zeros(self.local_swarms, dtype=cdt, **z)
+            self.d_best_perm = torch.zeros(n, dtype=torch.int16, **z)
+            self.d_best_cost = torch.zeros(1, dtype=cdt, **z)
+            self.d_best_iter = torch.zeros(1, dtype=torch.int64, **z)
+            self.d_best_idx = torch.zeros(1, dtype=torch.int64, **z)
+            self.d_iteration = torch.zeros(1, dtype=torch.int64, **z)
+            self.d_swarm_min = torch.zeros(self.local_swarms, dtype=cdt, **z)
+            self.d_swarm_min_idx = torch.zeros(self.local_swarms, dtype=torch.int64, **z)
+            self.d_done = torch.zeros(1, dtype=torch.int32, **z)
+        except torch.OutOfMemoryError:
+            raise MemoryError(
+                f"cannot allocate population buffers: {p} particles of size {n}x{n} need about "
+                f"{device_buffer_bytes(config, n)} bytes") from None
+        self.t = 0
+        self.pmf_range = (0.0, 1.0)
+        self._migration_log: list[MigrationEvent] = []
+        self._mig = None          # migration scratch, allocated on first use
+        self._host_best = None    # cached (cost, iteration, perm) of the device record
+        self._inst = None
+        self._coeffs_key = None
+
+    # ---------------------------------------------------------- C structs
+    def c_state(self) -> _lib.QsbState:
+        s = _lib.QsbState()
+        s.n, s.vstride, s.v_dtype, s.cost_dtype = self.n, self.vstride, self.v_code, self.cost_code
+        s.num_particles = self.local_particles
+        s.swarm_size = self.swarm_size
+        s.num_swarms = self.local_swarms
+        s.particle_offset = self.particle_offset
+        s.swarm_offset = self.swarm_offset
+        for name in ("V", "perm", "perm_new", "pl_perm", "cost", "pl_cost", "improved",
+                     "pg_perm", "pg_cost", "best_perm", "best_cost", "best_iter", "best_idx",
+                     "swarm_min", "swarm_min_idx", "done"):
+            setattr(s, name, _ptr(getattr(self, "d_" + name)))
+        s.iteration = _ptr(self.d_iteration)
+        return s
+
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def swap_positions(self):
+        self.d_perm, self.d_perm_new = self.d_perm_new, self.d_perm
+
+    @property
+    def migration_log(self) -> list:
+        _drain_log(self)
+        return self._migration_log
+
+    def swarm_of(self, particle: int) -> int:
+        return particle // self.swarm_size
+
+    # ------------------------------------------- reference-layout host views
+    def _mats(self, perms_t: torch.Tensor) -> np.ndarray:
+        p = perms_t.shape[0]
+        out = torch.empty((p, self.n, self.n), dtype=torch.int8, device=self.device)
+        if p:
+            _lib.call("qsb_perm_to_matrix", perms_t.data_ptr(), p, self.n, out.data_ptr(),
+                      self.stream())
+        return out.cpu().numpy()
+
+    @property
+    def X(self):
+        return self._mats(self.d_perm)
+
+    @property
+    def X_new(self):
+        return self._mats(self.d_perm_new)
+
+    @property
+    def PL(self):
+        return self._mats(self.d_pl_perm)
+
+    @property
+    def V(self):
+        p, nn = self.local_particles, self.n * self.n
+        return self.d_V[:, :nn].cpu().numpy().reshape(p, self.n, self.n)
+
+    @property
+    def perms(self):
+        return self.d_perm.cpu().numpy().astype(np.int64)
+
+    @property
+    def perms_new(self):
+        return self.d_perm_new.cpu().numpy().astype(np.int64)
+
+    @property
+    def pl_perms(self):
+        return self.d_pl_perm.cpu().numpy().astype(np.int64)
+
+    @property
+    def cost(self):
+        return self.d_cost.cpu().numpy()
+
+    @property
+    def pl_cost(self):
+        return self.d_pl_cost.cpu().numpy()
+
+    @property
+    def bests(self) -> SwarmBestTable:
+        return SwarmBestTable(matrices=self._mats(self.d_pg_perm),
+                              perms=self.d_pg_perm.cpu().numpy().astype(np.int64),
+                              costs=self.d_pg_cost.cpu().numpy())
+
+    def _best(self):
+        if self._host_best is None:
+            c = self.d_best_cost.cpu().numpy()[0].item()
+            it = int(self.d_best_iter.cpu()[0])
+            self._host_best = (c, it, self.d_best_perm.cpu().numpy().astype(np.int64))
+        return self._host_best
+
+    @property
+    def best_cost(self):
+        return self._best()[0]
+
+    @property
+    def best_iteration(self):
+        return self._best()[1]
+
+    @property
+    def best_perm(self):
+        return self._best()[2]
+
+
+# ---------------------------------------------------------------- runtime
+class _Runtime:
+    """Per-(state, instance, coefficients) C structs, rebuilt only on change."""
+
+    def __init__(self, state: PopulationState, instance, config: SolverConfig):
+        f, d, code = device_format(instance)
+        self.flow = torch.from_numpy(f.view(np.int16) if code == _lib.U16 else f).to(state.device)
+        self.dist = torch.from_numpy(d.view(np.int16) if code == _lib.U16 else d).to(state.device)
+        self.inst = _lib.QsbInstance(state.n, code, self.flow.data_ptr(), self.dist.data_ptr())
+        self.mat_code = code
+        self.key = (id(instance), config.coefficients, config.seed)
+        c = config.coefficients
+        self.coeffs = _lib.QsbCoeffs(c.c1, c.c2, c.c3, c.v_max, int(c.sv_mode == "norm"),
+                                     SX_CODES[c.sx_mode], c.depth, 0, int(config.seed) & (2**64 - 1))
+        if not _lib.lib().qsb_supported(state.n, state.v_code, code):
+            raise ValueError(f"problem size {state.n} is not supported by the fused kernel "
+                             f"at precision {config.precision}")
+
+
+def _runtime(state: PopulationState, instance, config: SolverConfig) -> _Runtime:
+    key = (id(instance), config.coefficients, config.seed)
+    rt = state._inst
+    if rt is None or rt.key != key:
+        rt = _Runtime(state, instance, config)
+        state._inst = rt
+    return rt
+
+
+# ----------------------------------------------------------------- init
+def _reference_init_arrays(config: SolverConfig, n: int):
+    """The reference's initial population (engine.py:150-156): row-wise
+    numpy ``permuted`` then ``uniform(-amp, amp)`` from init_rng(seed)."""
+    p = config.num_particles
+    rng = phase_rng(config.seed, PHASE_INIT, 0)
+    perms = rng.permuted(np.tile(np.arange(n, dtype=np.int64), (p, 1)), axis=1)
+    amp = config.init_velocity_amplitude
+    V = rng.uniform(-amp, amp, (p, n, n))
+    return perms, V
+
+
+def init_population(config: SolverConfig, instance, device=None, swarm_range=None) -> PopulationState:
+    """Seeded population: random permutations, uniform velocities; personal
+    bests = initial solutions; each swarm's best is its cheapest particle
+    (engine.py:139-178)."""
+    state = PopulationState(config, instance, device, swarm_range)
+    n, p = state.n, state.local_particles
+    lo_p = state.particle_offset
+    rt = _runtime(state, instance, config)
+    stream = state.stream()
+    if config.init == "reference":
+        perms, V = _reference_init_arrays(config, n)
+        perms = perms[lo_p:lo_p + p]
+        V = V[lo_p:lo_p + p]
+        state.d_perm.copy_(torch.from_numpy(perms.astype(np.int16)))
+        state.d_V[:, :n * n].copy_(torch.from_numpy(V.reshape(p, n * n)))
+        del V
+    else:
+        _lib.call("qsb_init_population_device", state.c_state(), int(config.seed) & (2**64 - 1),
+                  float(config.init_velocity_amplitude), stream)
+    _lib.call("qsb_cost", state.d_perm.data_ptr(), p, rt.inst, state.d_cost.data_ptr(), stream)
+    state.d_pl_perm.copy_(state.d_perm)
+    state.d_pl_cost.copy_(state.d_cost)
+    # swarm / global bests of the initial population = one best-kernel pass
+    # with every particle "improved" against +inf tables, at iteration 0
+    big = torch.finfo(torch.float64).max if not state.integral else torch.iinfo(torch.int64).max
+    state.d_pg_cost.fill_(big)
+    state.d_best_cost.fill_(big)
+    state.d_improved.fill_(1)
+    state.d_iteration.fill_(-1)
+    cs = state.c_state()
+    cs.perm_new = state.d_perm.data_ptr()
+    _lib.call("qsb_best_update", cs, stream)
+    state.t = 0
+    state._host_best = None
+    costs = state.d_cost.cpu().numpy()
+    if state.local_particles != state.num_particles and torch.distributed.is_initialized():
+        lo = torch.tensor([costs.min(), -costs.max()], dtype=torch.float64, device=state.device)
+        torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+        lo_v, hi_v = float(lo[0]), float(-lo[1])
+    else:
+        lo_v, hi_v = float(costs.min()), float(costs.max())
+    state.pmf_range = (lo_v, hi_v) if hi_v > lo_v else (lo_v, lo_v + 1.0)
+    return state
+
+
+# ------------------------------------------------------------- migration
+class _MigrationScratch:
+    def __init__(self, state: PopulationState, d: int):
+        dev = state.device
+        self.d = d
+        self.plan = torch.zeros((d, 4), dtype=torch.int64, device=dev)
+        self.log = torch.zeros((_LOG_EPOCHS, d, 6), dtype=torch.float64, device=dev)
+        self.log_count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.records = torch.zeros((d, state.n + 1), dtype=torch.int64, device=dev)
+        self.picks = None
+        self.picks_e0 = 0
+        self.pending = 0          # epochs logged on the device, not yet drained
+
+
+def migration_picks(seed: int, iteration: int, d: int, swarm_size: int) -> np.ndarray:
+    """Donor offsets of one migration event: ``host_rng(seed, t).integers(0, S)``
+    drawn once per replacement, in rank order (migration.py:82-84)."""
+    rng = phase_rng(seed, PHASE_HOST, iteration)
+    return np.array([rng.integers(0, swarm_size) for _ in range(d)], dtype=np.int32)
+
+
+def _drain_log(state: PopulationState):
+    ms = state._mig
+    if ms is None or ms.pending == 0:
+        return
+    rows = ms.log[:ms.pending].cpu().numpy().reshape(-1, 6)
+    for r in rows:
+        state._migration_log.append(MigrationEvent(int(r[0]), int(r[1]), int(r[2]), int(r[3]),
+                                                  float(r[4]), float(r[5])))
+    ms.log_count.zero_()
+    ms.pending = 0
+
+
+def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchange=None):
+    d = config.migration_depth
+    if state._mig is None or state._mig.d != d:
+        _drain_log(state)
+        state._mig = _MigrationScratch(state, d)
+    ms = state._mig
+    if ms.pending >= _LOG_EPOCHS:
+        _drain_log(state)
+    picks = torch.from_numpy(migration_picks(config.seed, t, d, state.swarm_size)).to(state.device)
+    ms.picks = picks
+    mig = _lib.QsbMigration()
+    mig.d, mig.period, mig.reserved = d, 0, 0
+    mig.num_swarms_total = state.swarms
+    mig.picks, mig.picks_epoch0, mig.picks_rows = picks.data_ptr(), t, 1
+    mig.plan, mig.records = ms.plan.data_ptr(), ms.records.data_ptr()
+    mig.log, mig.log_rows, mig.log_count = ms.log.data_ptr(), _LOG_EPOCHS, ms.log_count.data_ptr()
+    mig.status = ms.status.data_ptr()
+    stream = state.stream()
+    if exchange is None:
+        mig.mode = 0
+        mig.all_pg_cost = state.d_pg_cost.data_ptr()
+        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+    else:
+        exchange(state, mig, ms)
+    ms.pending += 1
+
+
+# ------------------------------------------------------------------ step
+def step(state: PopulationState, instance, config: SolverConfig, exchange=None) -> PopulationState:
+    """Advance one iteration (engine.py:181-244): the fused velocity /
+    aggregation / goal / personal-best kernel, the swarm and global best
+    reduction, the position swap and, when due, migration."""
+    coeffs = config.coefficients
+    n = state.n
+    if coeffs.sx_mode == "second-target" and not coeffs.depth < n:
+        raise ValueError(f"depth {coeffs.depth} must be below the problem size {n}")
+    t = state.t + 1
+    if not 0 <= t < _ITER_LIMIT:
+        raise ValueError(f"iteration {t} outside supported range")
+    rt = _runtime(state, instance, config)
+    stream = state.stream()
+    _lib.call("qsb_step", state.c_state(), rt.inst, rt.coeffs, stream)
+    state.swap_positions()
+    state._host_best = None
+    if config.migration_factor > 0.0 and t % config.migration_period == 0:
+        if config.migration_depth > 0:
+            _migrate_device(state, config, t, exchange)
+    state.t = t
+    return state
+
+
+@dataclass
+class RunResult:
+    """Outcome of a full run plus the collected statistics (engine.py:247-265)."""
+
+    instance_name: str
+    best_perm: np.ndarray
+    best_cost: float
+    best_iteration: int
+    gap: float | None
+    iterations_run: int
+    stats: list[IterationStats]
+    total_seconds: float
+    migration_events: list[MigrationEvent] = field(default_factory=list)
+
+    @property
+    def mean_ms_per_iteration(self) -> float:
+        if self.iterations_run == 0:
+            return 0.0
+        return 1000.0 * self.total_seconds / self.iterations_run
+
+
+def gap(cost: float, reference: float) -> float:
+    """(cost - reference) / reference (core.py:90-94)."""
+    if reference <= 0:
+        raise ValueError(f"reference must be positive, got {reference}")
+    return (cost - reference) / reference
+
+
+def run(config: SolverConfig, instance, collect_stats: bool = True, device=None) -> RunResult:
+    """Iterate until ``max_iterations`` or until the best reaches
+    ``target_cost`` (engine.py:268-307).  Statistics at iteration 0 and
+    every ``stats_stride``-th iteration."""
+    t_start = time.perf_counter()
+    state = init_population(config, instance, device)
+    series: list[IterationStats] = []
+    if collect_stats:
+        series.append(collect(state, 1000.0 * (time.perf_counter() - t_start),
+                              bins=config.pmf_bins, all_swarms=config.record_all_swarm_percentiles))
+    for _ in range(config.max_iterations):
+        if config.target_cost is not None and state.best_cost <= config.target_cost:
+            break
+        it_start = time.perf_counter()
+        step(state, instance, config)
+        if collect_stats and state.t % config.stats_stride == 0:
+            torch.cuda.current_stream(state.device).synchronize()
+            elapsed_ms = 1000.0 * (time.perf_counter() - it_start)
+            series.append(collect(state, elapsed_ms, bins=config.pmf_bins,
+                                  all_swarms=config.record_all_swarm_percentiles))
+    torch.cuda.current_stream(state.device).synchronize()
+    total = time.perf_counter() - t_start
+    _drain_log(state)
+    g = None
+    known = getattr(instance, "known_best", None)
+    if known is not None and known > 0:
+        g = gap(state.best_cost, known)
+    return RunResult(instance_name=getattr(instance, "name", ""), best_perm=state.best_perm.copy(),
+                     best_cost=state.best_cost, best_iteration=state.best_iteration, gap=g,
+                     iterations_run=state.t, stats=series, total_seconds=total,
+                     migration_events=list(state.migration_log))

@@ -1,0 +1,255 @@
+"""Parity of the CUDA path (libqsb.so) against the reference's golden vectors
+and the CPU oracle.  Integer/index results and the fp64 parity mode are
+compared bit for bit; the fp32 throughput mode with the column-scaled 1e-5
+rule of SURVEY.md A5."""
+
+import hashlib
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cuda_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+import paper_1504_05158_b200 as qsb            # noqa: E402
+from paper_1504_05158_b200 import batch         # noqa: E402
+from oracle import oracle as orc                # noqa: E402
+
+TRAJ_NAMES = ["A_chr12a_mig", "B_chr12a_raw_gm", "C_chr12a_pc_mig", "D_tai30_st_mig",
+              "E_float6", "F_tiny_gm", "G_zero_coeffs", "H_esc32e_st3", "I_tai50_norm"]
+
+
+def digest(state):
+    h = hashlib.sha256()
+    b = state.bests
+    for a in (state.X, state.V, state.PL, state.perms, state.cost, state.pl_cost,
+              b.matrices, b.costs):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def cfg_from(tr, **extra):
+    ck = dict(tr["coefficients"])
+    return qsb.SolverConfig(coefficients=qsb.PsoCoefficients(**ck), workers=2,
+                            **tr["config"], **extra)
+
+
+# ------------------------------------------------------------------ draws
+def test_step_draws_golden():
+    g = np.load(GOLDEN / "draws.npz")
+    for i, (seed, t, P, n) in enumerate(g["cases"].tolist()):
+        got = batch.step_draws(int(seed), int(t), int(P), int(n))
+        assert np.array_equal(got, g[f"case{i}"]), f"case {i}"
+
+
+# --------------------------------------------------------------- velocity
+def test_velocity_many_golden_bit_exact():
+    g = np.load(GOLDEN / "velocity.npz")
+    for k in range(int(g["count"])):
+        n, P, S, norm = g[f"v{k}_meta"].tolist()
+        c1, c2, c3, vmax = g[f"v{k}_coef"].tolist()
+        x = orc.matrices_from_perms(g[f"v{k}_perm"], n)
+        pl = orc.matrices_from_perms(g[f"v{k}_plperm"], n)
+        pg = orc.matrices_from_perms(g[f"v{k}_pgperm"], n)
+        v = g[f"v{k}_in"].copy()
+        batch.velocity_many(v, x, pl, pg, S, c1, c2 * g[f"v{k}_r2"], c3 * g[f"v{k}_r3"], vmax,
+                            bool(norm))
+        assert v.tobytes() == g[f"v{k}_out"].tobytes(), f"case {k}"
+
+
+@pytest.mark.parametrize("n", [2, 7, 31, 32, 33, 64, 65, 100, 128, 150])
+def test_velocity_many_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    P, S = 12, 4
+    x = orc.matrices_from_perms(np.array([rng.permutation(n) for _ in range(P)]), n)
+    pl = orc.matrices_from_perms(np.array([rng.permutation(n) for _ in range(P)]), n)
+    pg = orc.matrices_from_perms(np.array([rng.permutation(n) for _ in range(P // S)]), n)
+    v = rng.uniform(-5, 5, (P, n, n))
+    r2, r3 = rng.random(P), rng.random(P)
+    for norm in (False, True):
+        a, b = v.copy(), v.copy()
+        orc.velocity_many(a, x, pl, pg, S, 0.8, 0.5 * r2, 0.5 * r3, 4.0, norm)
+        batch.velocity_many(b, x, pl, pg, S, 0.8, 0.5 * r2, 0.5 * r3, 4.0, norm)
+        assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------ aggregation
+def test_aggregate_many_golden_bit_exact():
+    g = np.load(GOLDEN / "aggregate.npz")
+    for k in range(int(g["count"])):
+        mode, depth, n, p = g[f"a{k}_meta"].tolist()
+        x = orc.matrices_from_perms(g[f"a{k}_perm"], n)
+        out_mat = np.zeros_like(x)
+        out_perm = np.zeros((p, n), np.int64)
+        batch.aggregate_many(x, g[f"a{k}_v"], mode, depth, g[f"a{k}_draws"], out_mat, out_perm)
+        assert np.array_equal(out_perm, g[f"a{k}_out"]), f"case {k} mode {mode} n {n}"
+        assert np.array_equal(out_mat, orc.matrices_from_perms(out_perm, n))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("n", [2, 3, 5, 12, 31, 32, 33, 50, 64, 65, 100, 128, 129, 200])
+def test_aggregate_many_fuzz_vs_oracle(mode, n):
+    rng = np.random.default_rng(1000 * mode + n)
+    p = 24
+    perms = np.array([rng.permutation(n) for _ in range(p)])
+    x = orc.matrices_from_perms(perms, n)
+    kinds = [rng.uniform(-1, 1, (p, n, n)), rng.integers(-2, 3, (p, n, n)).astype(float),
+             np.zeros((p, n, n)), rng.integers(-1, 1, (p, n, n)).astype(float) * 0.25]
+    for depth in sorted({1, 2, min(3, n - 1), n - 1, n + 2}):
+        if mode == 2 and depth >= n and n > 2:
+            pass   # depth >= n is legal for the batched kernel (fallback path)
+        for v in kinds:
+            draws = rng.random((p, 2 * n))
+            a_mat, b_mat = np.zeros_like(x), np.zeros_like(x)
+            a_perm, b_perm = np.zeros((p, n), np.int64), np.zeros((p, n), np.int64)
+            orc.aggregate_many(x, v, mode, max(depth, 1), draws, a_mat, a_perm)
+            batch.aggregate_many(x, v, mode, max(depth, 1), draws, b_mat, b_perm)
+            assert np.array_equal(a_perm, b_perm), f"mode {mode} n {n} depth {depth}"
+
+
+# -------------------------------------------------------------------- cost
+def test_cost_many_golden(golden_instances):
+    g = np.load(GOLDEN / "cost.npz")
+    for name in ("chr12a", "tai30", "float6", "esc32e"):
+        inst = golden_instances[name]
+        perms = g[f"{name}_perms"]
+        out = np.zeros(perms.shape[0], g[f"{name}_cost"].dtype)
+        batch.cost_many(perms, inst.flow, inst.distance, out)
+        assert out.tobytes() == g[f"{name}_cost"].tobytes()
+
+
+def test_cost_many_wide_integers():
+    rng = np.random.default_rng(5)
+    n = 40
+    f = rng.integers(0, 2**31, (n, n))
+    d = rng.integers(0, 2**31, (n, n))
+    perms = np.array([rng.permutation(n) for _ in range(50)])
+    a = np.zeros(50, np.int64)
+    b = np.zeros(50, np.int64)
+    orc.cost_many(perms, f, d, a)
+    batch.cost_many(perms, f, d, b)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ trajectories
+@pytest.mark.parametrize("name", TRAJ_NAMES)
+def test_fp64_trajectory_bit_exact(name, trajectories, golden_instances):
+    tr = trajectories[name]
+    inst = golden_instances[tr["instance"]]
+    cfg = cfg_from(tr)
+    st = qsb.init_population(cfg, inst)
+    assert digest(st) == tr["digests"][0]
+    for t in range(tr["iterations"]):
+        qsb.step(st, inst, cfg)
+        assert digest(st) == tr["digests"][t + 1], f"step {t + 1}"
+        assert [st.best_cost, st.best_iteration] == tr["bests"][t + 1]
+    assert st.best_perm.tolist() == tr["best_perm"]
+    assert [list(e) for e in st.migration_log] == tr["migration_log"]
+
+
+def test_demo05_run_reproduces_golden_csv(golden_instances):
+    """pkg/demos/05_statistics.py config: stats.csv (minus wall time),
+    pmf.csv and solution.txt byte-identical to the reference's."""
+    inst = golden_instances["chr12a"]
+    config = qsb.SolverConfig(
+        swarms=50, swarm_size=50,
+        coefficients=qsb.PsoCoefficients(0.5, 0.5, 0.5, sv_mode="norm",
+                                         sx_mode="second-target", depth=2),
+        max_iterations=80, seed=11, workers=2, pmf_bins=40)
+    result = qsb.run(config, inst)
+    with tempfile.TemporaryDirectory() as d:
+        qsb.export_csv(result.stats, d)
+        qsb.write_solution(Path(d) / "solution.txt", inst.n, result.best_cost, result.best_perm)
+        stats = [",".join(r.split(",")[:-1]) for r in (Path(d) / "stats.csv").read_text().splitlines()]
+        assert "\n".join(stats) + "\n" == (GOLDEN / "demo05_stats_notime.csv").read_text()
+        assert (Path(d) / "pmf.csv").read_text() == (GOLDEN / "demo05_pmf.csv").read_text()
+        assert (Path(d) / "solution.txt").read_text() == (GOLDEN / "demo05_solution.txt").read_text()
+    assert result.best_cost == 9552 and result.best_iteration == 36
+
+
+def test_migration_period_extension(golden_instances):
+    """migration_period=K equals the oracle stepping with migration only when
+    t % K == 0 (the north-star's 'every 10 iterations')."""
+    inst = golden_instances["tai30"]
+    cfg = qsb.SolverConfig(swarms=6, swarm_size=10, seed=3, migration_factor=0.34,
+                           migration_period=3,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    st = qsb.init_population(cfg, inst)
+    ost = orc.init_population(6, 10, inst.n, inst.flow, inst.distance, seed=3)
+    kw = orc.coeff_kwargs(cfg)
+    for _ in range(9):
+        qsb.step(st, inst, cfg)
+        orc.step(ost, inst.flow, inst.distance, **kw)
+        assert np.array_equal(st.perms, ost.perms)
+        assert np.array_equal(st.bests.costs, ost.pg_costs)
+    assert len(st.migration_log) == 3 * cfg.migration_depth
+    assert [tuple(e) for e in st.migration_log] == [tuple(e) for e in ost.migration_log]
+
+
+# --------------------------------------------------------------- fp32 mode
+def test_fp32_velocity_column_scaled_tolerance(golden_instances):
+    inst = golden_instances["tai50"]
+    cfg = qsb.SolverConfig(swarms=20, swarm_size=25, seed=1, precision="fp32",
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    st = qsb.init_population(cfg, inst)
+    for _ in range(3):
+        qsb.step(st, inst, cfg)
+    # one more step from the GPU's own state, replayed on the oracle in f64
+    ost = orc.init_population(20, 25, inst.n, inst.flow, inst.distance, seed=1)
+    ost.X, ost.perms = st.X, st.perms
+    ost.PL, ost.pl_perms, ost.pl_cost = st.PL, st.pl_perms, st.pl_cost
+    b = st.bests
+    ost.pg_mats, ost.pg_perms, ost.pg_costs = b.matrices, b.perms, b.costs
+    ost.V = st.V.astype(np.float64)
+    ost.t = st.t
+    v_before = ost.V.copy()
+    qsb.step(st, inst, cfg)
+    orc.step(ost, inst.flow, inst.distance, **orc.coeff_kwargs(cfg))
+    got = st.V.astype(np.float64)
+    ref = ost.V
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    err = np.abs(got - ref) / np.where(scale > 0, scale, 1.0)
+    assert err.max() <= 1e-5, err.max()
+    # aggregation + goal are exact against the oracle fed the GPU's own V
+    x = orc.matrices_from_perms(np.asarray(ost.perms_new), inst.n)   # previous X (swapped)
+    draws = orc.step_draws(cfg.seed, st.t, cfg.num_particles, inst.n)
+    out_mat = np.zeros_like(x)
+    out_perm = np.zeros((cfg.num_particles, inst.n), np.int64)
+    orc.aggregate_many(x, np.ascontiguousarray(got), 2, 2, draws[:, 2:], out_mat, out_perm)
+    assert np.array_equal(out_perm, st.perms)
+    cost = np.zeros(cfg.num_particles, np.int64)
+    orc.cost_many(out_perm, inst.flow, inst.distance, cost)
+    assert np.array_equal(cost, st.cost)
+    del v_before
+
+
+# ------------------------------------------------- full-size properties
+def test_north_star_shape_properties():
+    """n=50, 80k particles (800 x 100), migration every 10 iterations:
+    size-independent invariants checked at full size."""
+    inst = qsb.taillard_uniform(50)
+    cfg = qsb.SolverConfig(swarms=800, swarm_size=100, seed=1, precision="fp32", init="device",
+                           migration_factor=0.33, migration_period=10,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    st = qsb.init_population(cfg, inst)
+    prev_pl = st.pl_cost
+    prev_best = st.best_cost
+    for _ in range(12):
+        qsb.step(st, inst, cfg)
+        perms = st.perms
+        assert (np.sort(perms, axis=1) == np.arange(50)).all()
+        pl = st.pl_cost
+        assert (pl <= prev_pl).all()
+        prev_pl = pl
+        assert st.best_cost <= prev_best
+        prev_best = st.best_cost
+    sample = np.random.default_rng(0).choice(cfg.num_particles, 500, replace=False)
+    c = np.zeros(500, np.int64)
+    orc.cost_many(perms[sample], inst.flow, inst.distance, c)
+    assert np.array_equal(c, st.cost[sample])
+    assert st.best_cost == orc.evaluate_cost(inst.flow, inst.distance, st.best_perm)
+    assert len(st.migration_log) == int(0.33 * 800)
