@@ -1,0 +1,387 @@
+"""Benchmark of the fused PSO step (BASELINE.json north-star workload).
+
+Workload (BASELINE.json configs[2]): synthetic Taillard-style QAP n=50,
+800 swarms x 100 particles (80k particles), c = (0.8, 0.5, 0.5), v_max 4,
+sv = norm, sx = second-target depth 2, migration factor 0.33 every 10
+iterations, seed 1, fp32 velocity state (the north-star throughput mode).
+A "step" is one PSO iteration over every particle.  Strong scaling: the 80k
+particles are split by swarms across the N ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Rank 0 prints one JSON line.  ``--impl reference`` times the CPU restatement
+of the reference's hot path (oracle/, kind "port") on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-iterations/sec (QAP n=50, 80k particles)"
+UNIT = "particle-iterations/s"
+N_DEFAULT, SWARMS, SWARM_SIZE = 50, 800, 100
+PERIOD, FACTOR, SEED = 10, 0.33, 1
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--swarms", type=int, default=SWARMS)
+    ap.add_argument("--swarm-size", type=int, default=SWARM_SIZE)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--velocity-only", action="store_true",
+                    help="time only the velocity/normalise phase of the fused kernel")
+    return ap.parse_args()
+
+
+def config(args, swarms=None, precision=None):
+    import paper_1504_05158_b200 as qsb
+    return qsb.SolverConfig(
+        swarms=swarms or args.swarms, swarm_size=args.swarm_size, seed=SEED,
+        coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5, v_max=4.0, sv_mode="norm",
+                                          sx_mode="second-target", depth=2),
+        migration_factor=FACTOR, migration_period=PERIOD,
+        precision=precision or args.precision, init="device")
+
+
+def workload(args, n_gpus):
+    return {"workload": f"synthetic Taillard-style QAP n={args.n}, {args.swarms} swarms x "
+                        f"{args.swarm_size} particles, migration f={FACTOR} every {PERIOD} "
+                        f"iterations, sv=norm, sx=second-target(2), c=(0.8,0.5,0.5)",
+            "n": args.n, "particles": args.swarms * args.swarm_size, "swarms": args.swarms,
+            "swarm_size": args.swarm_size, "precision": args.precision,
+            "parallelism": f"swarm-shard x{n_gpus}",
+            "l2": "inputs larger than L2 (velocity state "
+                  f"{args.swarms * args.swarm_size * args.n * args.n * (4 if args.precision == 'fp32' else 8) / 1e6:.0f} MB > 126 MB)"}
+
+
+def bytes_per_particle(n, S, sv):
+    """Algorithmic HBM bytes of the fused step per particle-iteration:
+    V read + write (2 n^2 sV), perm / pl_perm read + perm_new write (6n),
+    swarm best read amortised (2n/S), cost write, pl_cost read, improved
+    flag (17)."""
+    return 2 * n * n * sv + 6 * n + 2 * n / S + 17
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [int(r[0]) for r in rows]
+        load = [s for s in sm if s > 600] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": int(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# -------------------------------------------------------- kernel timer
+class KernelTimer:
+    """CUDA events around every fused-kernel launch on its own stream."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.pairs = []
+        self.active = False
+
+    def before(self, stream):
+        # the engine launches on torch's current stream (state.stream())
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.torch.cuda.current_stream())
+            self.pairs.append([e, None])
+
+    def after(self, stream):
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.torch.cuda.current_stream())
+            self.pairs[-1][1] = e
+
+    def mean_ms(self):
+        d = [a.elapsed_time(b) for a, b in self.pairs]
+        return sum(d) / len(d) if d else None
+
+
+def traffic_from_profile(n, precision, particles):
+    """ncu DRAM bytes per launch of the fused kernel, from profiles/ (or None)."""
+    p = ROOT / "profiles" / "ncu_step_summary.json"
+    if not p.exists():
+        return None
+    try:
+        rec = json.loads(p.read_text())
+        key = f"n{n}_{precision}_P{particles}"
+        return rec.get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------- CPU baseline
+def cpu_sample(args, seconds, swarms=8, steps_cap=1000, warm=1):
+    """The CPU restatement (oracle/, all host threads) on a bounded sample."""
+    import numpy as np
+    from oracle import oracle as orc
+    import paper_1504_05158_b200 as qsb
+    inst = qsb.taillard_uniform(args.n)
+    cfg = config(args, swarms=swarms, precision="fp64")
+    st = orc.init_population(cfg.swarms, cfg.swarm_size, args.n, inst.flow, inst.distance,
+                             seed=cfg.seed, amp=cfg.init_velocity_amplitude)
+    kw = orc.coeff_kwargs(cfg)
+    for _ in range(warm):
+        orc.step(st, inst.flow, inst.distance, **kw)
+    t0 = time.perf_counter()
+    k = 0
+    while k < steps_cap and (time.perf_counter() - t0) < seconds:
+        orc.step(st, inst.flow, inst.distance, **kw)
+        k += 1
+    dt = time.perf_counter() - t0
+    P = cfg.num_particles
+    return {"value": P * k / dt, "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
+            "sample": f"oracle/ (C+OpenMP restatement of the reference numba path, fp64, "
+                      f"O(n^3) aggregation as in _batch.py) on {cfg.swarms} swarms x "
+                      f"{cfg.swarm_size} particles of the same n={args.n} workload, {k} "
+                      f"iterations in {dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as orc
+    import paper_1504_05158_b200 as qsb
+    inst = qsb.taillard_uniform(args.n)
+    swarms = max(8, args.swarms // 10)
+    cfg = config(args, swarms=swarms, precision="fp64")
+    st = orc.init_population(cfg.swarms, cfg.swarm_size, args.n, inst.flow, inst.distance,
+                             seed=cfg.seed, amp=cfg.init_velocity_amplitude)
+    kw = orc.coeff_kwargs(cfg)
+    steps = min(args.steps, 30)
+    warm = min(args.warmup, 3)
+    for _ in range(warm):
+        orc.step(st, inst.flow, inst.distance, **kw)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        orc.step(st, inst.flow, inst.distance, **kw)
+    dt = time.perf_counter() - t0
+    P = cfg.num_particles
+    value = P * steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000 * dt / steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload(args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc.num_threads(),
+                             "kind": "port",
+                             "sample": f"{swarms} swarms x {cfg.swarm_size} particles per step "
+                                       f"(1/10 of the workload), fp64 reference arithmetic"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1504_05158_b200 as qsb
+    from paper_1504_05158_b200 import engine, shard
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    inst = qsb.taillard_uniform(args.n)
+    cfg = config(args)
+    lo, hi = shard.swarm_range(cfg.swarms, world, rank)
+    state = qsb.init_population(cfg, inst, device=dev, swarm_range=(lo, hi))
+    exchange = shard.make_exchange(world) if world > 1 else None
+    timer = KernelTimer()
+    flags = None
+    if args.velocity_only:
+        from paper_1504_05158_b200 import _lib
+        flags = _lib.PHASE_VELOCITY | _lib.PHASE_STORE_V
+
+    def one_step():
+        if flags is None:
+            qsb.step(state, inst, cfg, exchange=exchange, timer=timer)
+        else:
+            from paper_1504_05158_b200 import _lib
+            rt = engine._runtime(state, inst, cfg)
+            s = state.stream()
+            timer.before(s)
+            _lib.call("qsb_step_phases", state.c_state(), rt.inst, rt.coeffs, flags, None, 0, 2,
+                      None, 1, s)
+            timer.after(s)
+            state.launches += 1
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    stream = torch.cuda.current_stream()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = state.launches
+    timer.active = True
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    timer.active = False
+    clock_rec = clocks.stop() if clocks else None
+    ms = t_start.elapsed_time(t_end)
+    launches = state.launches - launches0
+    kern_ms = timer.mean_ms()
+    tm = torch.tensor([ms, kern_ms or 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms_max, kern_max = float(tm[0]), float(tm[1])
+    P_total = cfg.num_particles
+    value = P_total * args.steps / (ms_max / 1000.0)
+
+    # ---- end to end through the public API: step() + D2H of the step's
+    # per-particle costs and best record, synchronised every step
+    e2e_steps = args.e2e_steps if flags is None else 0
+    e2e = None
+    if e2e_steps:
+        host_cost = torch.empty(state.local_particles, dtype=state.d_cost.dtype, pin_memory=True)
+        host_best = torch.empty(1, dtype=state.d_best_cost.dtype, pin_memory=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            qsb.step(state, inst, cfg, exchange=exchange)
+            host_cost.copy_(state.d_cost, non_blocking=True)
+            host_best.copy_(state.d_best_cost, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        w = time.perf_counter() - w0
+        wt = torch.tensor([w], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        e2e = {"value": P_total * e2e_steps / float(wt[0]), "unit": UNIT,
+               "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(host_cost.numel() * host_cost.element_size()
+                                         + host_best.element_size()),
+               "steps": e2e_steps,
+               "how": "public step() per iteration + D2H of the iteration's cost vector and "
+                      "best cost (pinned), host-synchronised every step, wall clock, max over "
+                      "ranks; inputs are device-resident between iterations (no per-step "
+                      "host inputs exist: the random streams are generated in-kernel)"}
+
+    # ---- roofline of the fused kernel
+    sv = 4 if cfg.precision == "fp32" else 8
+    B = bytes_per_particle(args.n, args.swarm_size, sv)
+    if flags is not None:
+        B = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size
+    per_launch = B * state.local_particles
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = per_launch / (kern_max / 1000.0) / 1e9 if kern_max else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": traffic_from_profile(args.n, cfg.precision, state.local_particles),
+                "kernel": "step_kernel (fused velocity+aggregation+goal+pbest)" if flags is None
+                          else "step_kernel velocity-only build",
+                "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(args, args.cpu_seconds)
+
+    best = shard.merge_best(state.best_cost, state.best_iteration, 0, state.best_perm, world,
+                            dev) if world > 1 else None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32" if cfg.precision == "fp32" else "f64", "data": "synthetic",
+                "config": workload(args, world), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clock_rec,
+                "best_cost": best.cost if best else state.best_cost}
+        if flags is not None:
+            line["metric"] = "velocity/normalise phase HBM throughput"
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

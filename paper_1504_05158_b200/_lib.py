@@ -13,7 +13,7 @@ import subprocess
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libqsb.so"
+LIB_PATH = Path(os.environ.get("QSB_LIB", PKG / "libqsb.so"))
 HEADER = PKG.parent / "include" / "qapswarm_b200.h"
 
 QSB_OK, QSB_EINVAL, QSB_EUNSUPPORTED, QSB_ECUDA, QSB_EPERM = 0, 1, 2, 3, 4

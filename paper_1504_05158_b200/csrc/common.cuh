@@ -62,7 +62,9 @@ struct DrawRow {
     const uint64_t idx = base + (uint64_t)k;
     const uint64_t b = idx >> 2;
     if (b != cached) { blk = philox4x64_10(b + 1, seed, word1); cached = b; }
-    return u64_to_unit(blk.v[idx & 3]);
+    const unsigned l = (unsigned)(idx & 3);
+    const uint64_t w = l == 0 ? blk.v[0] : l == 1 ? blk.v[1] : l == 2 ? blk.v[2] : blk.v[3];
+    return u64_to_unit(w);
   }
 };
 
@@ -74,6 +76,11 @@ struct DrawRow {
 __device__ __forceinline__ uint64_t okey(double m) {
   const uint64_t b = (uint64_t)__double_as_longlong(m);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__device__ __forceinline__ double from_okey(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)b);
 }
 
 template <typename VT>

@@ -44,15 +44,15 @@ static size_t smem_optin() {
 }
 
 // ------------------------------------------------------------ fused step
-template <typename VT, typename MT, int G, int CPL, int W>
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 static int launch_step(const StepArgs& a, cudaStream_t s) {
-  using K = StepKernel<VT, MT, G, CPL, W>;
+  using K = StepKernel<VT, MT, G, CPL, W, GT>;
   StepArgs b = a;
   const bool need_fd = (a.flags & F_COST) != 0;
   b.fd_smem = need_fd && (G == 1 || K::smem_bytes(a.n, a.vstride, true) <= smem_optin());
   const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
-  auto fn = step_kernel<VT, MT, G, CPL, W>;
+  auto fn = step_kernel<VT, MT, G, CPL, W, GT>;
   static size_t attr_smem = 0;
   static size_t occ_smem = 0;
   static int occ_blocks = 0;
@@ -91,8 +91,9 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
     else return launch_step<VT, MT, 4, 1, 1>(a, s);
   }
   if (a.n <= 256) {
-    if constexpr (DRY) return StepKernel<VT, MT, 8, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
-    else return launch_step<VT, MT, 8, 1, 1>(a, s);
+    const bool fits = StepKernel<VT, MT, 8, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin();
+    if constexpr (DRY) return QSB_OK;
+    else return fits ? launch_step<VT, MT, 8, 1, 1>(a, s) : launch_step<VT, MT, 8, 1, 1, true>(a, s);
   }
   return QSB_EUNSUPPORTED;
 }

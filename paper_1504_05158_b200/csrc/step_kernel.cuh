@@ -6,17 +6,30 @@
 //
 //   * the velocity update and the column normalisation are column-local and
 //     run in the reference's exact order (_batch.py:39-58);
-//   * the aggregation keeps incremental per-column (max, count, first row)
-//     statistics over the free rows instead of the reference's O(n^3) rescan
-//     (_batch.py:89-175), reproducing its (max, tie-count) per round, its
-//     row-major k-th-tie selection and its draw consumption exactly;
+//   * the aggregation keeps incremental per-column statistics over the free
+//     rows instead of the reference's O(n^3) rescan (_batch.py:89-175),
+//     reproducing its (max, tie-count) per round, its row-major k-th-tie
+//     selection and its draw consumption exactly;
 //   * the QAP goal is a per-column partial sum over the smem-resident F, D
 //     (_batch.py:186-197), reduced in integer arithmetic.
+//
+// Aggregation statistics.  In column c the cell (zr, c), zr = perm[c], is
+// the only one with x = 1 ("z cell": m = 1 + v); every other cell has
+// m = 0 + v.  Each column therefore keeps
+//   - (nmax, ncnt, nrow): max / tie count / first row of v over its free
+//     non-z rows, compared directly in the velocity type (v1 > v2 on the
+//     stored values equals m1 > m2, and -0 == +0 as in m);
+//   - zkey: the ordered 64-bit key of 1 + v_z, and whether the z cell is
+//     currently eligible (its row free, and not inside the second-target
+//     restricted rounds).
+// The second-target restriction (_batch.py:90, 110) then only toggles z
+// eligibility, and a round costs O(CPL) per thread plus one warp reduction.
 //
 // The tile is staged global -> smem with one cp.async.bulk (1-D TMA) and the
 // updated velocity is written back with one bulk store, so the velocity
 // phase touches HBM exactly once in each direction.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace qsb {
@@ -63,6 +76,11 @@ struct Best {
   int row;
 };
 
+__device__ __forceinline__ Best best_none() {
+  Best b; b.key = 0; b.cnt = 0; b.col = INT_MAX; b.row = -1;
+  return b;
+}
+
 __device__ __forceinline__ Best best_merge(const Best& a, const Best& b) {
   if (a.key > b.key) return a;
   if (b.key > a.key) return b;
@@ -87,22 +105,56 @@ __device__ __forceinline__ Best warp_best(const Best& b) {
   return r;
 }
 
+// Fast path: when one lane holds the maximum high word, that lane's local
+// best is the answer (two shuffles); otherwise the full reduction.
+__device__ __forceinline__ Best warp_best_fast(const Best& b) {
+  const unsigned hi = (unsigned)(b.key >> 32);
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  const unsigned who = __ballot_sync(FULL, hi == mh && b.cnt > 0);
+  if (__popc(who) == 1) {
+    const int src = __ffs(who) - 1;
+    const unsigned pk = ((unsigned)b.cnt << 16) | ((unsigned)(b.col & 0xff) << 8) |
+                        (unsigned)((b.row + 1) & 0xff);
+    const unsigned lo = __shfl_sync(FULL, (unsigned)b.key, src);
+    const unsigned q = __shfl_sync(FULL, pk, src);
+    Best r;
+    r.key = ((uint64_t)mh << 32) | lo;
+    r.cnt = (int)(q >> 16);
+    r.col = (int)((q >> 8) & 0xff);
+    r.row = (int)(q & 0xff) - 1;
+    return r;
+  }
+  return warp_best(b);
+}
+
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
   return x;
 }
 
+// Position of the k-th (0-based) set bit of a 32-bit mask (k < popc(m)).
+__device__ __forceinline__ int nth_set_bit32(unsigned m, int k) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (k >= c) { k -= c; m >>= w; pos += w; }
+  }
+  return pos;
+}
+
 // Per-group shared scratch (one per particle group in the CTA).
 template <int NMAX, int G>
 struct GroupScratch {
   int sperm[NMAX];     // perm_new under construction (aggregation output)
-  int szr[NMAX];       // perm of the current position X (zero row per column)
-  int srow[NMAX];      // per-row tie counts / pick-column match flags
+  int szr[NMAX];       // perm of the current position X (z row per column)
+  int srow[NMAX];      // per-row tie counts / pick-column match flags / lists
   int sorder[NMAX];    // pick-column visiting order
-  unsigned char stie[NMAX];  // tied-column flags
+  unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
   Best slots[2][G];
-  int64_t lslots[2][G];
+  int islots[2][G];
+  int64_t lslots[G];
   int ssel[4];
   uint64_t bar;
 };
@@ -114,7 +166,11 @@ struct GroupSync {
   }
 };
 
-template <typename VT, typename MT, int G, int CPL, int W>
+#ifndef QSB_MINB
+#define QSB_MINB 1
+#endif
+
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 struct StepKernel {
   static constexpr int NT = 32 * G;          // threads per group
   static constexpr int NMAX = NT * CPL;      // largest n handled
@@ -125,7 +181,7 @@ struct StepKernel {
     return align_up(2 * (size_t)n * n * sizeof(MT), 128);
   }
   static __host__ __device__ size_t tile_bytes(int vstride) {
-    return align_up((size_t)vstride * sizeof(VT), 128);
+    return GT ? 0 : align_up((size_t)vstride * sizeof(VT), 128);
   }
   static __host__ __device__ size_t group_bytes(int vstride) {
     return tile_bytes(vstride) + align_up(sizeof(Scratch), 128);
@@ -135,15 +191,57 @@ struct StepKernel {
   }
 };
 
+// Group-wide best: warp fast path for one-warp groups, smem slots otherwise.
+template <int G, typename Scratch>
+__device__ __forceinline__ Best group_best(const Best& loc, Scratch& sc, int& par, int lane, int tid) {
+  if constexpr (G == 1) {
+    return warp_best_fast(loc);
+  } else {
+    Best b = warp_best(loc);
+    if (lane == 0) sc.slots[par][tid >> 5] = b;
+    __syncthreads();
+    b = sc.slots[par][0];
+#pragma unroll
+    for (int w = 1; w < G; ++w) b = best_merge(b, sc.slots[par][w]);
+    par ^= 1;
+    return b;
+  }
+}
+
+template <int G, typename Scratch>
+__device__ __forceinline__ int group_min_int(int x, Scratch& sc, int& ipar, int lane, int tid) {
+  x = __reduce_min_sync(FULL, x);
+  if constexpr (G > 1) {
+    if (lane == 0) sc.islots[ipar][tid >> 5] = x;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < G; ++w) x = min(x, sc.islots[ipar][w]);
+    ipar ^= 1;
+  }
+  return x;
+}
+
+template <typename VT>
+__device__ __forceinline__ uint64_t nonz_key(VT v) {   // key of m = 0.0 + v
+  return okey(__dadd_rn(0.0, (double)v));
+}
+template <typename VT>
+__device__ __forceinline__ uint64_t z_key(VT v) {      // key of m = 1.0 + v
+  return okey(__dadd_rn(1.0, (double)v));
+}
+
 // ------------------------------------------------------------------------
-template <typename VT, typename MT, int G, int CPL, int W>
-__global__ void __launch_bounds__(32 * G * W)
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
+__global__ void __launch_bounds__(32 * G * W, (G == 1 ? QSB_MINB : 1))
 step_kernel(const StepArgs a) {
-  using K = StepKernel<VT, MT, G, CPL, W>;
+  // GT: the particle tile stays in global memory (L1/L2-cached) instead of
+  // being staged in smem -- used when an n x n tile exceeds shared memory.
+  using K = StepKernel<VT, MT, G, CPL, W, GT>;
   constexpr int NT = K::NT;
   constexpr int NW = K::NW;
   using Scratch = typename K::Scratch;
   using Sync = GroupSync<G>;
+  constexpr bool kFloatMat = std::is_floating_point<MT>::value;
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
@@ -155,7 +253,7 @@ step_kernel(const StepArgs a) {
   const int tid = threadIdx.x % NT;
   const int lane = threadIdx.x & 31;
   unsigned char* gb = smem + (fds ? K::fd_bytes(n) : 0) + (size_t)gidx * K::group_bytes(a.vstride);
-  VT* tile = reinterpret_cast<VT*>(gb);
+  VT* tile = reinterpret_cast<VT*>(gb);   // re-pointed per particle when GT
   Scratch& sc = *reinterpret_cast<Scratch*>(gb + K::tile_bytes(a.vstride));
 
   const bool do_vel = a.flags & F_VELOCITY;
@@ -169,11 +267,10 @@ step_kernel(const StepArgs a) {
   if (do_cost) {
     const MT* gF = reinterpret_cast<const MT*>(a.F);
     const MT* gD = reinterpret_cast<const MT*>(a.D);
-    if constexpr (G == 1) {
+    if (G == 1 || fds) {
       for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
     } else {
-      if (fds) for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
-      else { cF = gF; cD = gD; }
+      cF = gF; cD = gD;
     }
   }
   if (tid == 0) { mbar_init(&sc.bar, 1); mbar_fence_init(); }
@@ -186,10 +283,13 @@ step_kernel(const StepArgs a) {
   const int64_t ngroups = (int64_t)gridDim.x * W;
   const int row_w = 2 + 2 * n;
   uint32_t phase = 0;
+  int par = 0, ipar = 0;
 
   for (int64_t p = (int64_t)blockIdx.x * W + gidx; p < a.P; p += ngroups) {
     VT* gV = reinterpret_cast<VT*>(a.V) + p * a.vstride;
-    if (tid == 0) {
+    if constexpr (GT) {
+      tile = gV;
+    } else if (tid == 0) {
       bulk_wait_read();                 // previous particle's store has left the tile
       mbar_arrive_expect_tx(&sc.bar, tile_bytes);
       bulk_load(tile, gV, tile_bytes, &sc.bar);
@@ -203,82 +303,139 @@ step_kernel(const StepArgs a) {
     dr.cached = ~0ULL;
 
     // ---- per-column registers
-    int zr[CPL], col[CPL];
+    int zr[CPL], col[CPL], plr[CPL], pgr[CPL];
     bool cfree[CPL];
-    uint64_t ckey[CPL];
-    int ccnt[CPL], crow[CPL];
     const int16_t* gperm = a.perm + p * n;
+    const int64_t s = p / a.S;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       col[k] = tid + k * NT;
       cfree[k] = col[k] < n;
       zr[k] = cfree[k] ? (int)gperm[col[k]] : -1;
       if (cfree[k]) sc.szr[col[k]] = zr[k];
-      ckey[k] = 0; ccnt[k] = 0; crow[k] = -1;
+      plr[k] = pgr[k] = -1;
+      if (do_vel && cfree[k]) {
+        plr[k] = a.pl_perm[p * n + col[k]];
+        pgr[k] = a.pg_perm[s * n + col[k]];
+      }
     }
-    const bool restricted0 = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
-
-    mbar_wait(&sc.bar, phase);
-    phase ^= 1u;
-
-    // ================= phase 1: velocity (+ initial column statistics)
+    double c2r2 = 0.0, c3r3 = 0.0;
     if (do_vel) {
-      double c2r2, c3r3;
       if (a.coef) { c2r2 = a.coef[2 * p]; c3r3 = a.coef[2 * p + 1]; }
       else {
         c2r2 = __dmul_rn(a.c2, dr.at(0));   // engine.py:198-199: c2 * r2, c3 * r3
         c3r3 = __dmul_rn(a.c3, dr.at(1));
       }
-      const int64_t s = p / a.S;
+    }
+
+    if constexpr (!GT) {
+      mbar_wait(&sc.bar, phase);
+      phase ^= 1u;
+    }
+
+    // ================= phase 1: velocity update (_batch.py:39-50)
+    VT total[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) total[k] = (VT)0;
+    if (do_vel) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
         const int c = col[k];
-        const int xr = zr[k];
-        const int plr = a.pl_perm[p * n + c];
-        const int pgr = a.pg_perm[s * n + c];
+        const int xr = zr[k], lr = plr[k], gr = pgr[k];
         if constexpr (sizeof(VT) == 8) {
-          // Reference order, no contraction: (c1*v + c2r2*(pl-x)) + c3r3*(pg-x)
-          double total = 0.0;
+          // reference order, no contraction: (c1*v + c2r2*(pl-x)) + c3r3*(pg-x)
+          const double z2 = __dmul_rn(c2r2, 0.0), z3 = __dmul_rn(c3r3, 0.0);
+          double tot = 0.0;
           for (int r = 0; r < n; ++r) {
             const double v = (double)tile[r * n + c];
-            const double d2 = (r == plr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
-            const double d3 = (r == pgr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
-            double lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), __dmul_rn(c2r2, d2)),
-                                   __dmul_rn(c3r3, d3));
+            double lin;
+            if (r == xr || r == lr || r == gr) {
+              const double d2 = (r == lr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
+              const double d3 = (r == gr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
+              lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), __dmul_rn(c2r2, d2)), __dmul_rn(c3r3, d3));
+            } else {
+              lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), z2), z3);
+            }
             if (lin > a.vmax) lin = a.vmax;
             else if (lin < -a.vmax) lin = -a.vmax;
             tile[r * n + c] = (VT)lin;
-            total = __dadd_rn(total, fabs(lin));
+            tot = __dadd_rn(tot, fabs(lin));
           }
-          if (a.normalize && total > 0.0)
-            for (int r = 0; r < n; ++r) tile[r * n + c] = (VT)__ddiv_rn((double)tile[r * n + c], total);
+          total[k] = (VT)tot;
         } else {
+          // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
+          // x / pl / pg are patched afterwards (sum order is not significant
+          // under the fp32 tolerance)
           const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
           const float vm = (float)a.vmax;
-          float total = 0.f;
+          const float vx = tile[xr * n + c], vl = tile[lr * n + c], vg = tile[gr * n + c];
+          float tot = 0.f;
+#pragma unroll 4
           for (int r = 0; r < n; ++r) {
-            const float v = (float)tile[r * n + c];
-            const float d2 = (float)((r == plr) - (r == xr));
-            const float d3 = (float)((r == pgr) - (r == xr));
-            float lin = fmaf(c3f, d3, fmaf(c2f, d2, c1f * v));
-            lin = fminf(fmaxf(lin, -vm), vm);
+            const float lin = fminf(fmaxf(c1f * (float)tile[r * n + c], -vm), vm);
             tile[r * n + c] = (VT)lin;
-            total += fabsf(lin);
+            tot += fabsf(lin);
           }
-          if (a.normalize && total > 0.f) {
-            const float inv = 1.0f / total;
-            for (int r = 0; r < n; ++r) tile[r * n + c] = (VT)((float)tile[r * n + c] * inv);
-          }
+          auto fix = [&](int r, float v0) {
+            const float d2 = (float)((r == lr) - (r == xr));
+            const float d3 = (float)((r == gr) - (r == xr));
+            const float g = fminf(fmaxf(c1f * v0, -vm), vm);
+            const float sp = fminf(fmaxf(fmaf(c3f, d3, fmaf(c2f, d2, c1f * v0)), -vm), vm);
+            tile[r * n + c] = (VT)sp;
+            tot += fabsf(sp) - fabsf(g);
+          };
+          fix(xr, vx);
+          if (lr != xr) fix(lr, vl);
+          if (gr != xr && gr != lr) fix(gr, vg);
+          total[k] = (VT)tot;
         }
       }
-      if (store_v) {
-        fence_proxy_async_smem();
-        Sync::sync();
-        if (tid == 0) bulk_store(gV, tile, tile_bytes);
-      } else {
-        Sync::sync();
+    }
+
+    // ================= normalisation (_batch.py:51-58) + initial statistics
+    VT nmax[CPL];
+    int ncnt[CPL], nrow[CPL];
+    uint64_t nk64[CPL], zkey[CPL];
+    bool zel[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      nmax[k] = (VT)0; ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
+      if (!cfree[k]) continue;
+      const int c = col[k];
+      const bool scale = do_vel && a.normalize && total[k] > (VT)0;
+      VT inv = (VT)1;
+      if constexpr (sizeof(VT) == 4) inv = scale ? 1.0f / total[k] : 1.0f;
+      if (do_agg) {
+        VT cur = (VT)0, zv = (VT)0;
+        int cn = 0, cr = -1;
+        for (int r = 0; r < n; ++r) {
+          VT v = tile[r * n + c];
+          if (scale) {
+            if constexpr (sizeof(VT) == 8) v = __ddiv_rn(v, total[k]);
+            else v = v * inv;
+            tile[r * n + c] = v;
+          }
+          if (r == zr[k]) { zv = v; continue; }
+          if (cn == 0 || v > cur) { cur = v; cn = 1; cr = r; }
+          else if (v == cur) ++cn;
+        }
+        nmax[k] = cur; ncnt[k] = cn; nrow[k] = cr;
+        nk64[k] = cn ? nonz_key(cur) : 0;
+        zkey[k] = z_key(zv);
+      } else if (scale) {
+        for (int r = 0; r < n; ++r) {
+          if constexpr (sizeof(VT) == 8) tile[r * n + c] = __ddiv_rn(tile[r * n + c], total[k]);
+          else tile[r * n + c] = tile[r * n + c] * inv;
+        }
       }
+    }
+    if (!GT && do_vel && store_v) {
+      fence_proxy_async_smem();
+      Sync::sync();
+      if (tid == 0) bulk_store(gV, tile, tile_bytes);
+    } else {
+      Sync::sync();
     }
 
     // ================= phase 2: aggregation S_x(X + V)
@@ -296,162 +453,171 @@ step_kernel(const StepArgs a) {
       int cursor = a.agg_base;     // next aggregation draw (column in the draw row)
 
       if (a.mode != MODE_PICK_COLUMN) {
-        bool restricted = restricted0;
-        // initial per-column statistics over all rows (skip z cells if restricted)
+        bool restricted = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          if (!cfree[k]) continue;
-          const int c = col[k];
-          uint64_t kk = 0; int cn = 0, cr = -1;
-          for (int r = 0; r < n; ++r) {
-            if (restricted && r == zr[k]) continue;
-            const uint64_t key = mval(r, c, zr[k]);
-            if (key > kk) { kk = key; cn = 1; cr = r; }
-            else if (key == kk) ++cn;
-          }
-          ckey[k] = kk; ccnt[k] = cn; crow[k] = cr;
-        }
+        for (int k = 0; k < CPL; ++k) zel[k] = cfree[k] && !restricted;
 
         for (int rnd = 0; rnd < n; ++rnd) {
           if (restricted && rnd == a.depth) {
-            // leaving the restricted phase: the z cells become candidates
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              if (!cfree[k] || !row_is_free(zr[k])) continue;
-              const uint64_t key = mval(zr[k], col[k], zr[k]);
-              if (key > ckey[k]) { ckey[k] = key; ccnt[k] = 1; crow[k] = zr[k]; }
-              else if (key == ckey[k]) { ++ccnt[k]; if (crow[k] >= 0 && zr[k] < crow[k]) crow[k] = zr[k]; }
-            }
+            // leaving the restricted rounds: free z cells become candidates
             restricted = false;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) zel[k] = cfree[k] && row_is_free(zr[k]);
           }
-          // ---- (max, count) over the eligible free cells
-          Best loc; loc.key = 0; loc.cnt = 0; loc.col = INT_MAX; loc.row = -1;
+          // ---- per-column combined candidate, then (max, count) over the group
+          uint64_t ck[CPL];
+          int cc[CPL], cr[CPL];
+          Best loc = best_none();
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
-            if (!cfree[k] || ccnt[k] == 0) continue;
-            Best b; b.key = ckey[k]; b.cnt = ccnt[k]; b.col = col[k]; b.row = crow[k];
-            loc = best_merge(loc, b);
+            ck[k] = 0; cc[k] = 0; cr[k] = -1;
+            if (!cfree[k]) continue;
+            const uint64_t nk = ncnt[k] ? nk64[k] : 0;
+            const uint64_t zk = zel[k] ? zkey[k] : 0;
+            if (nk > zk) { ck[k] = nk; cc[k] = ncnt[k]; cr[k] = nrow[k]; }
+            else if (zk > nk) { ck[k] = zk; cc[k] = 1; cr[k] = zr[k]; }
+            else if (nk != 0) {
+              ck[k] = zk; cc[k] = ncnt[k] + 1;
+              cr[k] = nrow[k] < 0 ? -1 : min(nrow[k], zr[k]);
+            }
+            if (cc[k]) {
+              Best b; b.key = ck[k]; b.cnt = cc[k]; b.col = col[k]; b.row = cr[k];
+              loc = best_merge(loc, b);
+            }
           }
-          Best b = warp_best(loc);
-          if constexpr (G > 1) {
-            const int par = rnd & 1;
-            if (lane == 0) sc.slots[par][tid >> 5] = b;
-            __syncthreads();
-            b = sc.slots[par][0];
-#pragma unroll
-            for (int w = 1; w < G; ++w) b = best_merge(b, sc.slots[par][w]);
-          }
+          const Best b = group_best<G>(loc, sc, par, lane, tid);
 
-          int sel_r, sel_c;
+          int sel_r = -1, sel_c = -1;
           if (b.cnt == 0) {
-            // every remaining cell is excluded (only a 1x1 remainder): the
+            // every remaining cell is excluded (a 1x1 remainder): the
             // reference falls back to the unrestricted set (_batch.py:118-132)
-            sel_r = -1;
 #pragma unroll
             for (int w = 0; w < NW; ++w)
               if (sel_r < 0 && rfree[w]) sel_r = w * 64 + __ffsll((long long)rfree[w]) - 1;
             int mc = INT_MAX;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) if (cfree[k]) mc = min(mc, col[k]);
-            mc = __reduce_min_sync(FULL, mc);
-            if constexpr (G > 1) {
-              if (lane == 0) sc.slots[rnd & 1][tid >> 5].col = mc;
-              __syncthreads();
-              for (int w = 0; w < G; ++w) mc = min(mc, sc.slots[rnd & 1][w].col);
-              __syncthreads();
-            }
-            sel_c = mc;
+            sel_c = group_min_int<G>(mc, sc, ipar, lane, tid);
           } else {
             int pick = 0;
             if (b.cnt > 1) {
               const double u = dr.at(cursor++);
-              long long pk = (long long)__dmul_rn(u, (double)b.cnt);
+              const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
             }
             if (b.cnt == 1 && b.row >= 0) {
               sel_r = b.row; sel_c = b.col;
             } else if (b.cnt == 1) {
-              // unique max, but that column's first row is not tracked: scan it
+              // unique maximum in column b.col whose first row is not tracked
               sel_c = b.col;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) if (col[k] == sel_c) sc.ssel[3] = zel[k];
+              Sync::sync();
+              const bool zok = sc.ssel[3];
               const int zc = sc.szr[sel_c];
               int found = INT_MAX;
 #pragma unroll
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
-                if (r < n && row_is_free(r) && !(restricted && r == zc) && mval(r, sel_c, zc) == b.key)
+                if (r < n && row_is_free(r) && (r != zc || zok) && mval(r, sel_c, zc) == b.key)
                   found = min(found, r);
               }
-              found = __reduce_min_sync(FULL, found);
-              if constexpr (G > 1) {
-                if (lane == 0) sc.slots[rnd & 1][tid >> 5].row = found;
-                __syncthreads();
-                for (int w = 0; w < G; ++w) found = min(found, sc.slots[rnd & 1][w].row);
-                __syncthreads();
-              }
-              sel_r = found;
+              sel_r = group_min_int<G>(found, sc, ipar, lane, tid);
+              Sync::sync();
             } else {
               // ---- ties: the pick-th tied cell in row-major order
+              bool fast = false;
+              if constexpr (G == 1 && CPL <= 2) {
+                // each tied column holds one tied cell with a known row: the
+                // row set is a 64-bit mask; distinct rows => the pick-th set
+                // bit is the answer (the common case: x cells tied at 1 + 0)
+                bool slow = false;
+                uint64_t rm = 0;
 #pragma unroll
-              for (int k = 0; k < CPL; ++k)
-                if (cfree[k] && ccnt[k] > 0 && ckey[k] == b.key) sc.stie[col[k]] = 1;
-              Sync::sync();
+                for (int k = 0; k < CPL; ++k) {
+                  if (cc[k] && ck[k] == b.key) {
+                    if (cc[k] == 1 && cr[k] >= 0) rm |= 1ULL << cr[k];
+                    else slow = true;
+                  }
+                }
+                const unsigned rl = __reduce_or_sync(FULL, (unsigned)rm);
+                const unsigned rh = __reduce_or_sync(FULL, (unsigned)(rm >> 32));
+                if (!__any_sync(FULL, slow) && __popc(rl) + __popc(rh) == b.cnt) {
+                  const int nl = __popc(rl);
+                  sel_r = pick < nl ? nth_set_bit32(rl, pick) : 32 + nth_set_bit32(rh, pick - nl);
+                  unsigned owner[CPL];
 #pragma unroll
-              for (int j = 0; j < CPL; ++j) {
-                const int r = tid + j * NT;
-                if (r >= n) continue;
-                int cnt = 0;
-                if (row_is_free(r)) {
+                  for (int k = 0; k < CPL; ++k)
+                    owner[k] = __ballot_sync(FULL, cc[k] && ck[k] == b.key && cr[k] == sel_r);
+                  sel_c = owner[0] ? __ffs(owner[0]) - 1 : 32 + __ffs(owner[CPL - 1]) - 1;
+                  fast = true;
+                }
+              }
+              if (!fast) {
+#pragma unroll
+                for (int k = 0; k < CPL; ++k)
+                  if (cc[k] && ck[k] == b.key) sc.stie[col[k]] = zel[k] ? 2 : 1;
+                Sync::sync();
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                  const int r = tid + j * NT;
+                  if (r >= n) continue;
+                  int cnt = 0;
+                  if (row_is_free(r)) {
+                    for (int c = 0; c < n; ++c) {
+                      const int tf = sc.stie[c];
+                      if (!tf) continue;
+                      const int zc = sc.szr[c];
+                      if (r == zc && tf != 2) continue;
+                      if (mval(r, c, zc) == b.key) ++cnt;
+                    }
+                  }
+                  sc.srow[r] = cnt;
+                }
+                Sync::sync();
+                if (tid == 0) {
+                  int r = 0, acc = 0;
+                  while (acc + sc.srow[r] <= pick) { acc += sc.srow[r]; ++r; }
+                  int q = pick - acc, cc2 = -1;
                   for (int c = 0; c < n; ++c) {
-                    if (!sc.stie[c]) continue;
+                    const int tf = sc.stie[c];
+                    if (!tf) continue;
                     const int zc = sc.szr[c];
-                    if (restricted && r == zc) continue;
-                    if (mval(r, c, zc) == b.key) ++cnt;
+                    if (r == zc && tf != 2) continue;
+                    if (mval(r, c, zc) == b.key) {
+                      if (q == 0) { cc2 = c; break; }
+                      --q;
+                    }
                   }
+                  sc.ssel[0] = r; sc.ssel[1] = cc2;
                 }
-                sc.srow[r] = cnt;
-              }
-              Sync::sync();
-              if (tid == 0) {
-                int r = 0, acc = 0;
-                while (acc + sc.srow[r] <= pick) { acc += sc.srow[r]; ++r; }
-                int q = pick - acc, cc = -1;
-                for (int c = 0; c < n; ++c) {
-                  if (!sc.stie[c]) continue;
-                  const int zc = sc.szr[c];
-                  if (restricted && r == zc) continue;
-                  if (mval(r, c, zc) == b.key) {
-                    if (q == 0) { cc = c; break; }
-                    --q;
-                  }
-                }
-                sc.ssel[0] = r; sc.ssel[1] = cc;
-              }
-              Sync::sync();
-              sel_r = sc.ssel[0]; sel_c = sc.ssel[1];
+                Sync::sync();
+                sel_r = sc.ssel[0]; sel_c = sc.ssel[1];
 #pragma unroll
-              for (int k = 0; k < CPL; ++k) if (cfree[k]) sc.stie[col[k]] = 0;
-              Sync::sync();
+                for (int k = 0; k < CPL; ++k) if (cfree[k]) sc.stie[col[k]] = 0;
+                Sync::sync();
+              }
             }
           }
 
-          // ---- retire row sel_r and column sel_c
+          // ---- retire row sel_r and column sel_c; update the statistics
           rfree[sel_r >> 6] &= ~(1ULL << (sel_r & 63));
           bool need[CPL];
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
             need[k] = false;
             if (!cfree[k]) continue;
-            if (col[k] == sel_c) { cfree[k] = false; sc.sperm[sel_c] = sel_r; continue; }
-            if (ccnt[k] == 0) continue;
-            if (restricted && zr[k] == sel_r) continue;
-            if (mval(sel_r, col[k], zr[k]) == ckey[k]) {
-              if (crow[k] == sel_r) crow[k] = -1;
-              if (--ccnt[k] == 0) need[k] = true;
+            if (col[k] == sel_c) { cfree[k] = false; zel[k] = false; sc.sperm[sel_c] = sel_r; continue; }
+            if (zr[k] == sel_r) { zel[k] = false; continue; }     // the retired cell is this column's z cell
+            if (ncnt[k] == 0) continue;
+            if (tile[sel_r * n + col[k]] == nmax[k]) {
+              if (nrow[k] == sel_r) nrow[k] = -1;
+              if (--ncnt[k] == 0) need[k] = true;
             }
           }
           if (rnd == n - 1) break;
 
-          // ---- cooperative rescans of columns whose maximum was retired
+          // ---- cooperative rescans of columns whose non-z maximum was retired
           if constexpr (G == 1) {
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
@@ -461,51 +627,55 @@ step_kernel(const StepArgs a) {
                 mask &= mask - 1;
                 const int c = src + k * 32;
                 const int zc = __shfl_sync(FULL, zr[k], src);
-                Best rb; rb.key = 0; rb.cnt = 0; rb.col = INT_MAX; rb.row = -1;
+                Best rb = best_none();
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
                   const int r = lane + j * 32;
-                  if (r >= n || !row_is_free(r) || (restricted && r == zc)) continue;
-                  const uint64_t key = mval(r, c, zc);
+                  if (r >= n || r == zc || !row_is_free(r)) continue;
+                  const uint64_t key = nonz_key(tile[r * n + c]);
                   if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                   else if (key == rb.key) ++rb.cnt;
                 }
                 const Best rr = warp_best(rb);
-                if (lane == src) { ckey[k] = rr.key; ccnt[k] = rr.cnt; crow[k] = rr.cnt ? rr.col : -1; }
+                if (lane == src) {
+                  ncnt[k] = rr.cnt;
+                  nrow[k] = rr.cnt ? rr.col : -1;
+                  nk64[k] = rr.cnt ? rr.key : 0;
+                  nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                }
               }
             }
           } else {
-            // generic group: list the columns, then scan each with all threads
             if (tid == 0) sc.ssel[2] = 0;
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              if (need[k]) sc.srow[atomicAdd(&sc.ssel[2], 1)] = k * NT + tid;
+              if (need[k]) sc.srow[atomicAdd(&sc.ssel[2], 1)] = col[k];
             __syncthreads();
             const int cnt = sc.ssel[2];
             for (int i = 0; i < cnt; ++i) {
               const int c = sc.srow[i];
               const int zc = sc.szr[c];
-              Best rb; rb.key = 0; rb.cnt = 0; rb.col = INT_MAX; rb.row = -1;
+              Best rb = best_none();
 #pragma unroll
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
-                if (r >= n || !row_is_free(r) || (restricted && r == zc)) continue;
-                const uint64_t key = mval(r, c, zc);
+                if (r >= n || r == zc || !row_is_free(r)) continue;
+                const uint64_t key = nonz_key(tile[r * n + c]);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
               }
-              Best rr = warp_best(rb);
-              const int par = (rnd + i + 1) & 1;
-              if (lane == 0) sc.slots[par][tid >> 5] = rr;
-              __syncthreads();
-              rr = sc.slots[par][0];
-              for (int w = 1; w < G; ++w) rr = best_merge(rr, sc.slots[par][w]);
+              const Best rr = group_best<G>(rb, sc, par, lane, tid);
 #pragma unroll
               for (int k = 0; k < CPL; ++k)
-                if (col[k] == c) { ckey[k] = rr.key; ccnt[k] = rr.cnt; crow[k] = rr.cnt ? rr.col : -1; }
-              __syncthreads();
+                if (col[k] == c) {
+                  ncnt[k] = rr.cnt;
+                  nrow[k] = rr.cnt ? rr.col : -1;
+                  nk64[k] = rr.cnt ? rr.key : 0;
+                  nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                }
             }
+            __syncthreads();
           }
         }
       } else {
@@ -526,7 +696,7 @@ step_kernel(const StepArgs a) {
         for (int rnd = 0; rnd < n; ++rnd) {
           const int c = sc.sorder[rnd];
           const int zc = sc.szr[c];
-          Best rb; rb.key = 0; rb.cnt = 0; rb.col = INT_MAX; rb.row = -1;
+          Best rb = best_none();
 #pragma unroll
           for (int j = 0; j < CPL; ++j) {
             const int r = tid + j * NT;
@@ -535,18 +705,11 @@ step_kernel(const StepArgs a) {
             if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
             else if (key == rb.key) ++rb.cnt;
           }
-          Best b = warp_best(rb);
-          if constexpr (G > 1) {
-            const int par = rnd & 1;
-            if (lane == 0) sc.slots[par][tid >> 5] = b;
-            __syncthreads();
-            b = sc.slots[par][0];
-            for (int w = 1; w < G; ++w) b = best_merge(b, sc.slots[par][w]);
-          }
+          const Best b = group_best<G>(rb, sc, par, lane, tid);
           int sel_r = b.col;   // first matching row
           if (b.cnt > 1) {
             const double u = dr.at(cursor++);
-            long long pk = (long long)__dmul_rn(u, (double)b.cnt);
+            const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
             const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
             // pick-th matching free row, ascending
 #pragma unroll
@@ -575,7 +738,7 @@ step_kernel(const StepArgs a) {
 
     // ================= phase 3: goal  sum_ij F[i,j] * D[perm_i, perm_j]
     if (do_cost) {
-      if constexpr (sizeof(MT) == 8 && (MT)0.5 != (MT)0) {
+      if constexpr (kFloatMat) {
         // non-integral instance: sequential i-major sum, as _batch.py:192-197
         if (tid == 0) {
           double acc = (double)cF[0] * (double)cD[0] * 0.0;
@@ -603,10 +766,10 @@ step_kernel(const StepArgs a) {
         }
         int64_t tot = warp_sum_i64((int64_t)part);
         if constexpr (G > 1) {
-          if (lane == 0) sc.lslots[0][tid >> 5] = tot;
+          if (lane == 0) sc.lslots[tid >> 5] = tot;
           __syncthreads();
           tot = 0;
-          for (int w = 0; w < G; ++w) tot += sc.lslots[0][w];
+          for (int w = 0; w < G; ++w) tot += sc.lslots[w];
         }
         if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;
       }
@@ -617,7 +780,7 @@ step_kernel(const StepArgs a) {
       Sync::sync();
       if (tid == 0) {
         bool imp;
-        if constexpr (sizeof(MT) == 8 && (MT)0.5 != (MT)0) {
+        if constexpr (kFloatMat) {
           const double cv = reinterpret_cast<double*>(a.cost)[p];
           double* pl = reinterpret_cast<double*>(a.pl_cost);
           imp = cv < pl[p];
@@ -639,7 +802,7 @@ step_kernel(const StepArgs a) {
     }
     Sync::sync();
   }
-  if (tid == 0) bulk_wait_all();
+  if (!GT && tid == 0) bulk_wait_all();
 }
 
 }  // namespace qsb

@@ -148,10 +148,15 @@ class PopulationState:
         self._mig = None          # migration scratch, allocated on first use
         self._host_best = None    # cached (cost, iteration, perm) of the device record
         self._inst = None
-        self._coeffs_key = None
+        self._cs = None
+        self.launches = 0         # kernels launched by step() (bench accounting)
 
     # ---------------------------------------------------------- C structs
     def c_state(self) -> _lib.QsbState:
+        s = self._cs
+        if s is not None:
+            s.perm, s.perm_new = self.d_perm.data_ptr(), self.d_perm_new.data_ptr()
+            return s
         s = _lib.QsbState()
         s.n, s.vstride, s.v_dtype, s.cost_dtype = self.n, self.vstride, self.v_code, self.cost_code
         s.num_particles = self.local_particles
@@ -164,6 +169,7 @@ class PopulationState:
                      "swarm_min", "swarm_min_idx", "done"):
             setattr(s, name, _ptr(getattr(self, "d_" + name)))
         s.iteration = _ptr(self.d_iteration)
+        self._cs = s
         return s
 
     def stream(self):
@@ -339,17 +345,37 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
 
 # ------------------------------------------------------------- migration
 class _MigrationScratch:
+    """Device buffers of the migration phase plus a window of precomputed
+    donor picks (one row of d offsets per migration epoch)."""
+
+    CHUNK = 64
+
     def __init__(self, state: PopulationState, d: int):
         dev = state.device
         self.d = d
+        self.device = dev
         self.plan = torch.zeros((d, 4), dtype=torch.int64, device=dev)
         self.log = torch.zeros((_LOG_EPOCHS, d, 6), dtype=torch.float64, device=dev)
         self.log_count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.records = torch.zeros((d, state.n + 1), dtype=torch.int64, device=dev)
         self.picks = None
-        self.picks_e0 = 0
+        self.e0 = 0
+        self.rows = 0
         self.pending = 0          # epochs logged on the device, not yet drained
+
+    def ensure_picks(self, config: SolverConfig, t: int, swarm_size: int):
+        """Make sure the picks window holds epoch t // period."""
+        period = config.migration_period
+        e = t // period
+        if self.picks is not None and self.e0 <= e < self.e0 + self.rows:
+            return
+        last = (_ITER_LIMIT - 1) // period
+        rows = max(1, min(self.CHUNK, last - e + 1))
+        tab = np.stack([migration_picks(config.seed, (e + r) * period, self.d, swarm_size)
+                        for r in range(rows)])
+        self.picks = torch.from_numpy(tab).to(self.device)
+        self.e0, self.rows = e, rows
 
 
 def migration_picks(seed: int, iteration: int, d: int, swarm_size: int) -> np.ndarray:
@@ -366,12 +392,13 @@ def _drain_log(state: PopulationState):
     rows = ms.log[:ms.pending].cpu().numpy().reshape(-1, 6)
     for r in rows:
         state._migration_log.append(MigrationEvent(int(r[0]), int(r[1]), int(r[2]), int(r[3]),
-                                                  float(r[4]), float(r[5])))
+                                                   float(r[4]), float(r[5])))
     ms.log_count.zero_()
     ms.pending = 0
 
 
-def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchange=None):
+def migration_struct(state: PopulationState, config: SolverConfig, t: int) -> _lib.QsbMigration:
+    """C descriptor of the migration event at iteration t (picks prepared)."""
     d = config.migration_depth
     if state._mig is None or state._mig.d != d:
         _drain_log(state)
@@ -379,30 +406,37 @@ def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchan
     ms = state._mig
     if ms.pending >= _LOG_EPOCHS:
         _drain_log(state)
-    picks = torch.from_numpy(migration_picks(config.seed, t, d, state.swarm_size)).to(state.device)
-    ms.picks = picks
+    ms.ensure_picks(config, t, state.swarm_size)
     mig = _lib.QsbMigration()
-    mig.d, mig.period, mig.reserved = d, 0, 0
+    mig.d, mig.period, mig.mode, mig.reserved = d, config.migration_period, 0, 0
     mig.num_swarms_total = state.swarms
-    mig.picks, mig.picks_epoch0, mig.picks_rows = picks.data_ptr(), t, 1
+    mig.picks, mig.picks_epoch0, mig.picks_rows = ms.picks.data_ptr(), ms.e0, ms.rows
+    mig.all_pg_cost = state.d_pg_cost.data_ptr()
     mig.plan, mig.records = ms.plan.data_ptr(), ms.records.data_ptr()
     mig.log, mig.log_rows, mig.log_count = ms.log.data_ptr(), _LOG_EPOCHS, ms.log_count.data_ptr()
     mig.status = ms.status.data_ptr()
-    stream = state.stream()
+    return mig
+
+
+def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchange=None):
+    mig = migration_struct(state, config, t)
     if exchange is None:
-        mig.mode = 0
-        mig.all_pg_cost = state.d_pg_cost.data_ptr()
-        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+        _lib.call("qsb_migrate", state.c_state(), mig, state.stream())
     else:
-        exchange(state, mig, ms)
-    ms.pending += 1
+        exchange(state, mig)
+    state._mig.pending += 1
 
 
 # ------------------------------------------------------------------ step
-def step(state: PopulationState, instance, config: SolverConfig, exchange=None) -> PopulationState:
+def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
+         timer=None) -> PopulationState:
     """Advance one iteration (engine.py:181-244): the fused velocity /
     aggregation / goal / personal-best kernel, the swarm and global best
-    reduction, the position swap and, when due, migration."""
+    reduction, the position swap and, when due, migration.
+
+    ``exchange`` performs the cross-device part of migration when the
+    swarms are sharded (see shard.py); ``timer`` (optional) brackets the
+    fused kernel launch with CUDA events for roofline measurement."""
     coeffs = config.coefficients
     n = state.n
     if coeffs.sx_mode == "second-target" and not coeffs.depth < n:
@@ -412,12 +446,21 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None) 
         raise ValueError(f"iteration {t} outside supported range")
     rt = _runtime(state, instance, config)
     stream = state.stream()
-    _lib.call("qsb_step", state.c_state(), rt.inst, rt.coeffs, stream)
+    cs = state.c_state()
+    if timer is not None:
+        timer.before(stream)
+    _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, _lib.PHASE_ALL, None, 0, 2, None, 0,
+              stream)
+    if timer is not None:
+        timer.after(stream)
+    _lib.call("qsb_best_update", cs, stream)
+    state.launches += 2
     state.swap_positions()
     state._host_best = None
     if config.migration_factor > 0.0 and t % config.migration_period == 0:
         if config.migration_depth > 0:
             _migrate_device(state, config, t, exchange)
+            state.launches += 1 if exchange is None else 2
     state.t = t
     return state
 

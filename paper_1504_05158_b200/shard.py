@@ -1,0 +1,111 @@
+"""Swarm sharding across the GPUs of one node (one process per GPU).
+
+Each rank owns a contiguous block of swarms, hence a contiguous range of
+GLOBAL particle ids; the in-kernel random streams are keyed by global ids,
+so any world size reproduces the single-device trajectory bit for bit.
+
+The data path needs no collective inside an iteration.  Cross-rank traffic
+happens only at:
+
+* migration epochs (migration.py:55-86 semantics, every
+  ``migration_period`` iterations): all-gather of the m swarm-best costs
+  (m x 8 B), every rank ranks them identically on the device and packs the
+  donor records it owns, one all-reduce(sum) of the d x (n+1) record buffer
+  (28.6 KB at n=50, d=264), then each rank applies the records of the
+  swarms it owns;
+* the global best (engine.py:225-229): an all-gather of each rank's
+  (cost, first iteration, global particle id, permutation) record and a
+  lexicographic minimum, which reproduces the reference's strict-< /
+  first-index rule because ranks own ascending id ranges.
+
+The collective sequence is written against ``torch.distributed`` so the
+same code runs over NCCL (GPU tensors) and gloo (CPU tensors, used by the
+world-size-2 tests with CPU stand-ins for the pack/apply kernels).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def swarm_range(swarms: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced block of swarms owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid rank / world size")
+    if swarms < world:
+        raise ValueError(f"cannot shard {swarms} swarms over {world} ranks")
+    base, extra = divmod(swarms, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def gather_swarm_costs(local: torch.Tensor, swarms: int, world: int, group=None) -> torch.Tensor:
+    """All-gather the per-rank swarm-best cost blocks into global order."""
+    if world == 1:
+        return local
+    sizes = [swarm_range(swarms, world, r) for r in range(world)]
+    width = max(hi - lo for lo, hi in sizes)
+    buf = torch.zeros(width, dtype=local.dtype, device=local.device)
+    buf[:local.numel()] = local
+    out = torch.empty(world * width, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return torch.cat([out[r * width: r * width + (hi - lo)] for r, (lo, hi) in enumerate(sizes)])
+
+
+def exchange_records(records: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the donor-record buffers: each donor row is non-zero on exactly
+    one rank (its owner), so the sum is the full record set."""
+    dist.all_reduce(records, op=dist.ReduceOp.SUM, group=group)
+    return records
+
+
+def make_exchange(world: int, group=None):
+    """Cross-device migration hook for ``engine.step(..., exchange=...)``."""
+    from . import _lib
+
+    def exchange(state, mig):
+        full = gather_swarm_costs(state.d_pg_cost, state.swarms, world, group)
+        mig.all_pg_cost = full.data_ptr()
+        stream = state.stream()
+        mig.mode = 1
+        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+        exchange_records(state._mig.records, group)
+        mig.mode = 2
+        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+        state._keep_alive = full
+
+    return exchange
+
+
+@dataclass
+class BestRecord:
+    cost: float
+    iteration: int
+    index: int
+    perm: np.ndarray
+
+
+def merge_best(cost, iteration: int, index: int, perm, world: int, device, group=None,
+               integral: bool = True) -> BestRecord:
+    """Global best over ranks: lexicographic min of (cost, iteration, index)."""
+    n = len(perm)
+    rec = torch.zeros(4 + n, dtype=torch.float64 if not integral else torch.int64, device=device)
+    rec[0] = cost
+    rec[1] = iteration
+    rec[2] = index
+    rec[4:] = torch.as_tensor(np.asarray(perm), dtype=rec.dtype)
+    if world > 1:
+        out = torch.empty(world * (4 + n), dtype=rec.dtype, device=device)
+        dist.all_gather_into_tensor(out, rec, group=group)
+        rows = out.view(world, 4 + n).cpu().numpy()
+    else:
+        rows = rec.view(1, 4 + n).cpu().numpy()
+    best = min(range(rows.shape[0]), key=lambda r: (rows[r, 0], rows[r, 1], rows[r, 2]))
+    r = rows[best]
+    c = r[0].item()
+    return BestRecord(int(c) if integral else float(c), int(r[1]), int(r[2]),
+                      r[4:].astype(np.int64))
