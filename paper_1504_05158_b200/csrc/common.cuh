@@ -78,6 +78,15 @@ __device__ __forceinline__ uint64_t okey(double m) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
 }
 
+__device__ __forceinline__ unsigned okey32(float f) {
+  const unsigned b = __float_as_uint(f);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ float from_okey32(unsigned k) {
+  return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
+}
+
 __device__ __forceinline__ double from_okey(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
   return __longlong_as_double((long long)b);

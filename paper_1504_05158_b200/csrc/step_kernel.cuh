@@ -152,6 +152,7 @@ struct GroupScratch {
   int srow[NMAX];      // per-row tie counts / pick-column match flags / lists
   int sorder[NMAX];    // pick-column visiting order
   unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
+  uint64_t sbulk[NMAX];      // z keys assigned by bulk steps (pending tie-draw count)
   Best slots[2][G];
   int islots[2][G];
   int64_t lslots[G];
@@ -167,7 +168,7 @@ struct GroupSync {
 };
 
 #ifndef QSB_MINB
-#define QSB_MINB 1
+#define QSB_MINB 4
 #endif
 
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
@@ -454,37 +455,177 @@ step_kernel(const StepArgs a) {
 
       if (a.mode != MODE_PICK_COLUMN) {
         bool restricted = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
+        // cached per-column candidate: (key, tie count, first row) of the
+        // column's best eligible cell; recomputed only when its parts change
+        uint64_t ck[CPL];
+        int cc[CPL], cr[CPL];
+        auto recompute = [&](int k) {
+          const uint64_t nk = ncnt[k] ? nk64[k] : 0;
+          const uint64_t zk = zel[k] ? zkey[k] : 0;
+          if (nk > zk) { ck[k] = nk; cc[k] = ncnt[k]; cr[k] = nrow[k]; }
+          else if (zk > nk) { ck[k] = zk; cc[k] = 1; cr[k] = zr[k]; }
+          else {
+            ck[k] = zk;
+            cc[k] = zk ? ncnt[k] + 1 : 0;
+            cr[k] = nrow[k] < 0 ? -1 : min(nrow[k], zr[k]);
+          }
+        };
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) zel[k] = cfree[k] && !restricted;
+        for (int k = 0; k < CPL; ++k) {
+          zel[k] = cfree[k] && !restricted;
+          ck[k] = 0; cc[k] = 0; cr[k] = -1;
+          if (cfree[k]) recompute(k);
+        }
+
+        // G == 1: rescan (cooperatively, lanes = rows) every column whose
+        // non-z maximum left; the owner lane stores the new statistics
+        auto warp_rescans = [&](const bool (&need)[CPL]) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              unsigned mask = __ballot_sync(FULL, need[k]);
+              while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int c = src + k * 32;
+                const int zc = __shfl_sync(FULL, zr[k], src);
+                if constexpr (sizeof(VT) == 4) {
+                  // fp32: one 32-bit key per cell, three warp reductions
+                  unsigned km = 0, kc = 0, kr = INT_MAX;
+#pragma unroll
+                  for (int j = 0; j < CPL; ++j) {
+                    const int r = lane + j * 32;
+                    if (r >= n || r == zc || !row_is_free(r)) continue;
+                    const unsigned key = okey32(__fadd_rn((float)tile[r * n + c], 0.0f));
+                    if (key > km) { km = key; kc = 1; kr = r; }
+                    else if (key == km) ++kc;
+                  }
+                  const unsigned M = __reduce_max_sync(FULL, km);
+                  const bool match = km == M && kc > 0;
+                  const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
+                  const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
+                  if (lane == src) {
+                    ncnt[k] = (int)tot;
+                    nrow[k] = tot ? (int)rr : -1;
+                    nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
+                    nk64[k] = tot ? nonz_key(nmax[k]) : 0;
+                    recompute(k);
+                  }
+                } else {
+                  Best rb = best_none();
+#pragma unroll
+                  for (int j = 0; j < CPL; ++j) {
+                    const int r = lane + j * 32;
+                    if (r >= n || r == zc || !row_is_free(r)) continue;
+                    const uint64_t key = nonz_key(tile[r * n + c]);
+                    if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
+                    else if (key == rb.key) ++rb.cnt;
+                  }
+                  const Best rr = warp_best(rb);
+                  if (lane == src) {
+                    ncnt[k] = rr.cnt;
+                    nrow[k] = rr.cnt ? rr.col : -1;
+                    nk64[k] = rr.cnt ? rr.key : 0;
+                    nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                    recompute(k);
+                  }
+                }
+              }
+            }
+        };
+        // bulk z-cell assignment bookkeeping (G == 1): keys of z cells placed
+        // in bulk steps, whose tie-draw count is settled lazily
+        int nbulk = 0;
+        auto settle_bulk = [&]() {
+          if (nbulk == 0) return;
+          int firsts = 0;
+          for (int i = lane; i < nbulk; i += 32) {
+            const uint64_t ki = sc.sbulk[i];
+            bool first = true;
+            for (int j = 0; j < i; ++j) if (sc.sbulk[j] == ki) { first = false; break; }
+            firsts += first;
+          }
+          const int distinct = (int)__reduce_add_sync(FULL, (unsigned)firsts);
+          cursor += nbulk - distinct;
+          nbulk = 0;
+          __syncwarp();
+        };
 
         for (int rnd = 0; rnd < n; ++rnd) {
           if (restricted && rnd == a.depth) {
             // leaving the restricted rounds: free z cells become candidates
             restricted = false;
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) zel[k] = cfree[k] && row_is_free(zr[k]);
+            for (int k = 0; k < CPL; ++k)
+              if (cfree[k]) { zel[k] = row_is_free(zr[k]); recompute(k); }
           }
-          // ---- per-column combined candidate, then (max, count) over the group
-          uint64_t ck[CPL];
-          int cc[CPL], cr[CPL];
-          Best loc = best_none();
+          // ---- bulk step (unrestricted rounds, G == 1): every free z cell
+          // whose m = 1 + v exceeds the largest free non-z cell is selected
+          // before any non-z cell, in some order that does not change the
+          // result; a group of g equal keys costs g - 1 tie draws.  Assign
+          // them all at once instead of one round each.
+          if constexpr (G == 1 && CPL <= 2) {
+            if (!restricted) {
+              uint64_t ml = 0;
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            ck[k] = 0; cc[k] = 0; cr[k] = -1;
-            if (!cfree[k]) continue;
-            const uint64_t nk = ncnt[k] ? nk64[k] : 0;
-            const uint64_t zk = zel[k] ? zkey[k] : 0;
-            if (nk > zk) { ck[k] = nk; cc[k] = ncnt[k]; cr[k] = nrow[k]; }
-            else if (zk > nk) { ck[k] = zk; cc[k] = 1; cr[k] = zr[k]; }
-            else if (nk != 0) {
-              ck[k] = zk; cc[k] = ncnt[k] + 1;
-              cr[k] = nrow[k] < 0 ? -1 : min(nrow[k], zr[k]);
-            }
-            if (cc[k]) {
-              Best b; b.key = ck[k]; b.cnt = cc[k]; b.col = col[k]; b.row = cr[k];
-              loc = best_merge(loc, b);
+              for (int k = 0; k < CPL; ++k)
+                if (cfree[k] && ncnt[k] && nk64[k] > ml) ml = nk64[k];
+              const unsigned mh = __reduce_max_sync(FULL, (unsigned)(ml >> 32));
+              const unsigned mlo = __reduce_max_sync(FULL, (unsigned)(ml >> 32) == mh ? (unsigned)ml : 0u);
+              const uint64_t M = ((uint64_t)mh << 32) | mlo;
+              bool q[CPL];
+              unsigned qb[CPL];
+              int nq = 0;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) {
+                q[k] = cfree[k] && zel[k] && zkey[k] > M;
+                qb[k] = __ballot_sync(FULL, q[k]);
+                nq += __popc(qb[k]);
+              }
+              if (nq >= 2) {
+                const unsigned lt = (1u << lane) - 1u;
+                uint64_t rbits = 0;
+                int base = nbulk;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                  if (q[k]) {
+                    sc.sbulk[base + __popc(qb[k] & lt)] = zkey[k];
+                    sc.sperm[col[k]] = zr[k];
+                    rbits |= 1ULL << zr[k];
+                    cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
+                  }
+                  base += __popc(qb[k]);
+                }
+                nbulk = base;
+                __syncwarp();
+                const unsigned rl = __reduce_or_sync(FULL, (unsigned)rbits);
+                const unsigned rh = __reduce_or_sync(FULL, (unsigned)(rbits >> 32));
+                const uint64_t rmask = ((uint64_t)rh << 32) | rl;
+                rfree[0] &= ~rmask;
+                rnd += nq - 1;
+                if (rnd >= n - 1) break;
+                // non-z statistics whose maximum row may have left
+                bool need[CPL];
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                  need[k] = false;
+                  if (!cfree[k] || !ncnt[k]) continue;
+                  if (ncnt[k] == 1 && nrow[k] >= 0) need[k] = (rmask >> nrow[k]) & 1ULL;
+                  else need[k] = true;
+                }
+                warp_rescans(need);
+                continue;
+              }
             }
           }
+          // ---- lane-local best of the cached candidates, then the group's
+          Best loc;
+          loc.key = ck[0]; loc.cnt = cc[0]; loc.col = col[0]; loc.row = cr[0];
+#pragma unroll
+          for (int k = 1; k < CPL; ++k) {
+            if (ck[k] > loc.key) { loc.key = ck[k]; loc.cnt = cc[k]; loc.col = col[k]; loc.row = cr[k]; }
+            else if (ck[k] == loc.key) loc.cnt += cc[k];
+          }
+          if (loc.cnt == 0) { loc.key = 0; loc.col = INT_MAX; }
           const Best b = group_best<G>(loc, sc, par, lane, tid);
 
           int sel_r = -1, sel_c = -1;
@@ -501,6 +642,7 @@ step_kernel(const StepArgs a) {
           } else {
             int pick = 0;
             if (b.cnt > 1) {
+              if constexpr (G == 1) settle_bulk();
               const double u = dr.at(cursor++);
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
@@ -607,44 +749,27 @@ step_kernel(const StepArgs a) {
           for (int k = 0; k < CPL; ++k) {
             need[k] = false;
             if (!cfree[k]) continue;
-            if (col[k] == sel_c) { cfree[k] = false; zel[k] = false; sc.sperm[sel_c] = sel_r; continue; }
-            if (zr[k] == sel_r) { zel[k] = false; continue; }     // the retired cell is this column's z cell
-            if (ncnt[k] == 0) continue;
-            if (tile[sel_r * n + col[k]] == nmax[k]) {
-              if (nrow[k] == sel_r) nrow[k] = -1;
-              if (--ncnt[k] == 0) need[k] = true;
+            if (col[k] == sel_c) {
+              cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
+              sc.sperm[sel_c] = sel_r;
+              continue;
             }
+            bool chg = false;
+            if (zr[k] == sel_r) {                     // this column's z cell left
+              chg = zel[k];
+              zel[k] = false;
+            } else if (ncnt[k] && tile[sel_r * n + col[k]] == nmax[k]) {
+              if (nrow[k] == sel_r) nrow[k] = -1;
+              need[k] = --ncnt[k] == 0;
+              chg = true;
+            }
+            if (chg) recompute(k);
           }
           if (rnd == n - 1) break;
 
           // ---- cooperative rescans of columns whose non-z maximum was retired
           if constexpr (G == 1) {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              unsigned mask = __ballot_sync(FULL, need[k]);
-              while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int c = src + k * 32;
-                const int zc = __shfl_sync(FULL, zr[k], src);
-                Best rb = best_none();
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                  const int r = lane + j * 32;
-                  if (r >= n || r == zc || !row_is_free(r)) continue;
-                  const uint64_t key = nonz_key(tile[r * n + c]);
-                  if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
-                  else if (key == rb.key) ++rb.cnt;
-                }
-                const Best rr = warp_best(rb);
-                if (lane == src) {
-                  ncnt[k] = rr.cnt;
-                  nrow[k] = rr.cnt ? rr.col : -1;
-                  nk64[k] = rr.cnt ? rr.key : 0;
-                  nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
-                }
-              }
-            }
+            warp_rescans(need);
           } else {
             if (tid == 0) sc.ssel[2] = 0;
             __syncthreads();
@@ -673,6 +798,7 @@ step_kernel(const StepArgs a) {
                   nrow[k] = rr.cnt ? rr.col : -1;
                   nk64[k] = rr.cnt ? rr.key : 0;
                   nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                  recompute(k);
                 }
             }
             __syncthreads();
