@@ -97,6 +97,8 @@ typedef struct qsb_instance {
   int32_t mat_dtype;         /* QSB_U16, QSB_I64 or QSB_F64 */
   const void* flow;          /* (n, n) row-major */
   const void* distance;      /* (n, n) row-major */
+  int32_t acc32;             /* 1 if n * max(flow) * max(distance) < 2^32 (caller-checked) */
+  int32_t reserved;
 } qsb_instance;
 
 /* kernels.PsoCoefficients (kernels.py:47-76) plus the run seed. */
@@ -105,9 +107,13 @@ typedef struct qsb_coeffs {
   int32_t normalize;         /* sv_mode == "norm" */
   int32_t sx_mode;           /* QSB_SX_* */
   int32_t depth;
-  int32_t reserved;
+  int32_t hints;             /* QSB_HINT_* bits (caller-guaranteed properties) */
   uint64_t seed;             /* SolverConfig.seed wrapped to uint64 (streams.py:34) */
 } qsb_coeffs;
+
+/* |c1 * v| <= v_max holds for every stored velocity entry, so the clamp of
+ * the rows untouched by x / pl / pg is a no-op and may be skipped. */
+#define QSB_HINT_V_BOUNDED 1
 
 /* One migration event (migration.migrate, migration.py:55-86). */
 typedef struct qsb_migration {

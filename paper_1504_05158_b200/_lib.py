@@ -19,6 +19,7 @@ HEADER = PKG.parent / "include" / "qapswarm_b200.h"
 QSB_OK, QSB_EINVAL, QSB_EUNSUPPORTED, QSB_ECUDA, QSB_EPERM = 0, 1, 2, 3, 4
 F32, F64, I64, U16 = 1, 2, 3, 4
 PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 4, 8, 16
+HINT_V_BOUNDED = 1
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V
 
 _vp = ctypes.c_void_p
@@ -42,12 +43,13 @@ class QsbState(ctypes.Structure):
 
 
 class QsbInstance(ctypes.Structure):
-    _fields_ = [("n", _i32), ("mat_dtype", _i32), ("flow", _vp), ("distance", _vp)]
+    _fields_ = [("n", _i32), ("mat_dtype", _i32), ("flow", _vp), ("distance", _vp),
+                ("acc32", _i32), ("reserved", _i32)]
 
 
 class QsbCoeffs(ctypes.Structure):
     _fields_ = [("c1", _dbl), ("c2", _dbl), ("c3", _dbl), ("v_max", _dbl),
-                ("normalize", _i32), ("sx_mode", _i32), ("depth", _i32), ("reserved", _i32),
+                ("normalize", _i32), ("sx_mode", _i32), ("depth", _i32), ("hints", _i32),
                 ("seed", _u64)]
 
 

@@ -166,6 +166,8 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.improved = st->improved;
   a.F = inst ? inst->flow : nullptr;
   a.D = inst ? inst->distance : nullptr;
+  a.acc32 = inst ? inst->acc32 : 0;
+  a.v_bounded = (co->hints & QSB_HINT_V_BOUNDED) ? 1 : 0;
 }
 
 int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co,

@@ -67,6 +67,8 @@ struct StepArgs {
   int agg_base;              // column of the first aggregation draw in a row
   const double* coef;        // optional (P, 2): c2*r2, c3*r3 per particle
   int fd_smem;               // 1: stage F, D in smem; 0: read them from global/L2
+  int v_bounded;             // host guarantee: |c1 * v| <= v_max for every stored v
+  int acc32;                 // host guarantee: n * max(F) * max(D) < 2^32
 };
 
 struct Best {
@@ -358,8 +360,10 @@ step_kernel(const StepArgs a) {
             } else {
               lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), z2), z3);
             }
-            if (lin > a.vmax) lin = a.vmax;
-            else if (lin < -a.vmax) lin = -a.vmax;
+            if (!a.v_bounded || r == xr || r == lr || r == gr) {
+              if (lin > a.vmax) lin = a.vmax;
+              else if (lin < -a.vmax) lin = -a.vmax;
+            }
             tile[r * n + c] = (VT)lin;
             tot = __dadd_rn(tot, fabs(lin));
           }
@@ -372,11 +376,21 @@ step_kernel(const StepArgs a) {
           const float vm = (float)a.vmax;
           const float vx = tile[xr * n + c], vl = tile[lr * n + c], vg = tile[gr * n + c];
           float tot = 0.f;
+          if (a.v_bounded) {
+            // |c1 v| <= v_max is guaranteed for every stored v: no clamp
 #pragma unroll 4
-          for (int r = 0; r < n; ++r) {
-            const float lin = fminf(fmaxf(c1f * (float)tile[r * n + c], -vm), vm);
-            tile[r * n + c] = (VT)lin;
-            tot += fabsf(lin);
+            for (int r = 0; r < n; ++r) {
+              const float lin = c1f * (float)tile[r * n + c];
+              tile[r * n + c] = (VT)lin;
+              tot += fabsf(lin);
+            }
+          } else {
+#pragma unroll 4
+            for (int r = 0; r < n; ++r) {
+              const float lin = fminf(fmaxf(c1f * (float)tile[r * n + c], -vm), vm);
+              tile[r * n + c] = (VT)lin;
+              tot += fabsf(lin);
+            }
           }
           auto fix = [&](int r, float v0) {
             const float d2 = (float)((r == lr) - (r == xr));
@@ -408,8 +422,13 @@ step_kernel(const StepArgs a) {
       VT inv = (VT)1;
       if constexpr (sizeof(VT) == 4) inv = scale ? 1.0f / total[k] : 1.0f;
       if (do_agg) {
-        VT cur = (VT)0, zv = (VT)0;
+        // branchless max / tie count / first row over the non-z rows; the z
+        // row is masked to -inf (all stored values are finite)
+        const VT NINF = (VT)(-INFINITY);
+        const int zrk = zr[k];
+        VT cur = NINF, zv = (VT)0;
         int cn = 0, cr = -1;
+#pragma unroll 2
         for (int r = 0; r < n; ++r) {
           VT v = tile[r * n + c];
           if (scale) {
@@ -417,9 +436,13 @@ step_kernel(const StepArgs a) {
             else v = v * inv;
             tile[r * n + c] = v;
           }
-          if (r == zr[k]) { zv = v; continue; }
-          if (cn == 0 || v > cur) { cur = v; cn = 1; cr = r; }
-          else if (v == cur) ++cn;
+          const bool isz = r == zrk;
+          zv = isz ? v : zv;
+          const VT w = isz ? NINF : v;
+          const bool gt = w > cur;
+          cn = gt ? 1 : cn + ((w == cur && !isz) ? 1 : 0);
+          cr = gt ? r : cr;
+          cur = gt ? w : cur;
         }
         nmax[k] = cur; ncnt[k] = cn; nrow[k] = cr;
         nk64[k] = cn ? nonz_key(cur) : 0;
@@ -882,12 +905,21 @@ step_kernel(const StepArgs a) {
           const int j = col[k];
           if (j >= n) continue;
           const int pj = sc.sperm[j];
-          for (int i = 0; i < n; ++i) {
-            const int pi = sc.sperm[i];
-            if constexpr (sizeof(MT) <= 2)
-              part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[pi * n + pj]);
-            else
-              part += (uint64_t)cF[i * n + j] * (uint64_t)cD[pi * n + pj];
+          if constexpr (sizeof(MT) <= 2) {
+            if (a.acc32) {
+              // n * max(F) * max(D) < 2^32: the column sum fits 32 bits
+              uint32_t p32 = 0;
+#pragma unroll 4
+              for (int i = 0; i < n; ++i)
+                p32 += (uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj];
+              part += p32;
+            } else {
+              for (int i = 0; i < n; ++i)
+                part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj]);
+            }
+          } else {
+            for (int i = 0; i < n; ++i)
+              part += (uint64_t)cF[i * n + j] * (uint64_t)cD[sc.sperm[i] * n + pj];
           }
         }
         int64_t tot = warp_sum_i64((int64_t)part);

@@ -150,6 +150,7 @@ class PopulationState:
         self._inst = None
         self._cs = None
         self.launches = 0         # kernels launched by step() (bench accounting)
+        self.v_bound = float("inf")   # proven bound on max |V| (enables QSB_HINT_V_BOUNDED)
 
     # ---------------------------------------------------------- C structs
     def c_state(self) -> _lib.QsbState:
@@ -266,7 +267,11 @@ class _Runtime:
         f, d, code = device_format(instance)
         self.flow = torch.from_numpy(f.view(np.int16) if code == _lib.U16 else f).to(state.device)
         self.dist = torch.from_numpy(d.view(np.int16) if code == _lib.U16 else d).to(state.device)
-        self.inst = _lib.QsbInstance(state.n, code, self.flow.data_ptr(), self.dist.data_ptr())
+        acc32 = 0
+        if code == _lib.U16:
+            acc32 = int(state.n * int(f.max()) * int(d.max()) < 2**32)
+        self.inst = _lib.QsbInstance(state.n, code, self.flow.data_ptr(), self.dist.data_ptr(),
+                                     acc32, 0)
         self.mat_code = code
         self.key = (id(instance), config.coefficients, config.seed)
         c = config.coefficients
@@ -332,6 +337,7 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
     _lib.call("qsb_best_update", cs, stream)
     state.t = 0
     state._host_best = None
+    state.v_bound = float(config.init_velocity_amplitude)
     costs = state.d_cost.cpu().numpy()
     if state.local_particles != state.num_particles and torch.distributed.is_initialized():
         lo = torch.tensor([costs.min(), -costs.max()], dtype=torch.float64, device=state.device)
@@ -447,6 +453,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     rt = _runtime(state, instance, config)
     stream = state.stream()
     cs = state.c_state()
+    # |c1 v| <= v_max for every stored v => the bulk-row clamp is a no-op
+    rt.coeffs.hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
     if timer is not None:
         timer.before(stream)
     _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, _lib.PHASE_ALL, None, 0, 2, None, 0,
@@ -455,6 +463,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
         timer.after(stream)
     _lib.call("qsb_best_update", cs, stream)
     state.launches += 2
+    # after S_v every entry is clamped to v_max, or normalised to |v| <= 1
+    state.v_bound = (1.0 + 1e-6) if coeffs.sv_mode == "norm" else coeffs.v_max
     state.swap_positions()
     state._host_best = None
     if config.migration_factor > 0.0 and t % config.migration_period == 0:
