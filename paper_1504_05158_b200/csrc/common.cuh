@@ -37,6 +37,13 @@ __device__ __forceinline__ PhiloxBlock philox4x64_10(uint64_t c0, uint64_t k0, u
   return b;
 }
 
+// Out-of-line copy for the per-particle draw rows: the block is evaluated a
+// few times per particle, and inlining 10 rounds at every call site bloats
+// the step kernel beyond the instruction cache.
+__device__ __noinline__ PhiloxBlock philox_block_call(uint64_t c0, uint64_t k0, uint64_t k1) {
+  return philox4x64_10(c0, k0, k1);
+}
+
 __device__ __forceinline__ double u64_to_unit(uint64_t u) {
   return (double)(u >> 11) * (1.0 / 9007199254740992.0);
 }
@@ -61,7 +68,7 @@ struct DrawRow {
     if (inj) return inj[k];
     const uint64_t idx = base + (uint64_t)k;
     const uint64_t b = idx >> 2;
-    if (b != cached) { blk = philox4x64_10(b + 1, seed, word1); cached = b; }
+    if (b != cached) { blk = philox_block_call(b + 1, seed, word1); cached = b; }
     const unsigned l = (unsigned)(idx & 3);
     const uint64_t w = l == 0 ? blk.v[0] : l == 1 ? blk.v[1] : l == 2 ? blk.v[2] : blk.v[3];
     return u64_to_unit(w);

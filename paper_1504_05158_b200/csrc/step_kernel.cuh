@@ -233,6 +233,204 @@ __device__ __forceinline__ uint64_t z_key(VT v) {      // key of m = 1.0 + v
   return okey(__dadd_rn(1.0, (double)v));
 }
 
+// Set of free rows (bit r of word r/64).
+template <int NW>
+struct RowSet {
+  uint64_t w[NW];
+  __device__ __forceinline__ bool has(int r) const { return (w[r >> 6] >> (r & 63)) & 1ULL; }
+  __device__ __forceinline__ void clear(int r) { w[r >> 6] &= ~(1ULL << (r & 63)); }
+  __device__ __forceinline__ int first() const {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) if (w[i]) return i * 64 + __ffsll((long long)w[i]) - 1;
+    return -1;
+  }
+};
+
+template <typename VT>
+__device__ __forceinline__ uint64_t mkey(const VT* tile, int n, int r, int c, int zrc) {
+  return okey(cell_m(tile[r * n + c], r == zrc));
+}
+
+// ---- rare paths, kept out of line so the round loop stays in I-cache ----
+
+// Group-wide int minimum with its own barriers (callable from any point).
+template <int G, typename Scratch>
+__device__ __forceinline__ int group_min_sync(int x, Scratch& sc, int lane, int tid) {
+  x = __reduce_min_sync(FULL, x);
+  if constexpr (G > 1) {
+    __syncthreads();
+    if (lane == 0) sc.islots[0][tid >> 5] = x;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < G; ++w) x = min(x, sc.islots[0][w]);
+    __syncthreads();
+  }
+  return x;
+}
+
+// Tie round: the pick-th tied cell in row-major order (_batch.py:155-170).
+// Owners have flagged the tied columns in sc.stie (2 = its z cell is
+// eligible) before the call.  Result in sc.ssel[0..1]; flags cleared.
+template <typename VT, int G, int NW, typename Scratch>
+__device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc, RowSet<NW> rf,
+                                             uint64_t key, int pick, int tid) {
+  constexpr int NT = 32 * G;
+  GroupSync<G>::sync();
+  for (int r = tid; r < n; r += NT) {
+    int cnt = 0;
+    if (rf.has(r)) {
+      for (int c = 0; c < n; ++c) {
+        const int tf = sc.stie[c];
+        if (!tf) continue;
+        const int zc = sc.szr[c];
+        if (r == zc && tf != 2) continue;
+        if (mkey(tile, n, r, c, zc) == key) ++cnt;
+      }
+    }
+    sc.srow[r] = cnt;
+  }
+  GroupSync<G>::sync();
+  if (tid == 0) {
+    int r = 0, acc = 0;
+    while (acc + sc.srow[r] <= pick) { acc += sc.srow[r]; ++r; }
+    int q = pick - acc, cc = -1;
+    for (int c = 0; c < n; ++c) {
+      const int tf = sc.stie[c];
+      if (!tf) continue;
+      const int zc = sc.szr[c];
+      if (r == zc && tf != 2) continue;
+      if (mkey(tile, n, r, c, zc) == key) {
+        if (q == 0) { cc = c; break; }
+        --q;
+      }
+    }
+    sc.ssel[0] = r; sc.ssel[1] = cc;
+  }
+  GroupSync<G>::sync();
+  for (int c = tid; c < n; c += NT) sc.stie[c] = 0;
+}
+
+// Unique maximum in column c whose first row is not tracked: scan it.
+template <typename VT, int G, int CPL, int NW, typename Scratch>
+__device__ __noinline__ int first_row_scan(const VT* tile, int n, Scratch& sc, RowSet<NW> rf,
+                                           uint64_t key, int c, bool zok, int tid, int lane) {
+  constexpr int NT = 32 * G;
+  const int zc = sc.szr[c];
+  int found = INT_MAX;
+  for (int r = tid; r < n; r += NT)
+    if (rf.has(r) && (r != zc || zok) && mkey(tile, n, r, c, zc) == key) found = min(found, r);
+  return group_min_sync<G>(found, sc, lane, tid);
+}
+
+// Number of distinct keys among the z cells placed by bulk steps.
+template <typename Scratch>
+__device__ __noinline__ int bulk_distinct(const Scratch& sc, int nb, int lane) {
+  int firsts = 0;
+  for (int i = lane; i < nb; i += 32) {
+    const uint64_t ki = sc.sbulk[i];
+    bool first = true;
+    for (int j = 0; j < i; ++j) if (sc.sbulk[j] == ki) { first = false; break; }
+    firsts += first;
+  }
+  return (int)__reduce_add_sync(FULL, (unsigned)firsts);
+}
+
+// pick-column S_x (_batch.py:78-88, 93-102, 145-153): Fisher-Yates column
+// order from n-1 draws, then per column the max over the free rows with
+// uniform tie-breaking in row order.  Writes sc.sperm.
+template <typename VT, int G, int NW, typename Scratch>
+__device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc, RowSet<NW> rf,
+                                             DrawRow dr, int cursor, int tid, int lane) {
+  constexpr int NT = 32 * G;
+  GroupSync<G>::sync();
+  for (int i = tid; i < n; i += NT) sc.sorder[i] = i;
+  GroupSync<G>::sync();
+  if (tid == 0) {
+    for (int i = n - 1; i > 0; --i) {
+      const double u = dr.at(cursor++);
+      long long j = (long long)__dmul_rn(u, (double)(i + 1));
+      if (j > i) j = i;
+      const int tmp = sc.sorder[i]; sc.sorder[i] = sc.sorder[j]; sc.sorder[j] = tmp;
+    }
+    sc.ssel[3] = cursor;
+  }
+  GroupSync<G>::sync();
+  cursor = sc.ssel[3];
+  int par = 0;
+  for (int rnd = 0; rnd < n; ++rnd) {
+    const int c = sc.sorder[rnd];
+    const int zc = sc.szr[c];
+    Best rb = best_none();
+    for (int r = tid; r < n; r += NT) {
+      if (!rf.has(r)) continue;
+      const uint64_t key = mkey(tile, n, r, c, zc);
+      if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
+      else if (key == rb.key) ++rb.cnt;
+    }
+    const Best b = group_best<G>(rb, sc, par, lane, tid);
+    int sel_r = b.col;   // first matching row
+    if (b.cnt > 1) {
+      const double u = dr.at(cursor++);
+      const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
+      const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
+      for (int r = tid; r < n; r += NT)
+        sc.srow[r] = (rf.has(r) && mkey(tile, n, r, c, zc) == b.key) ? 1 : 0;
+      GroupSync<G>::sync();
+      if (tid == 0) {
+        int q = pick, r = 0;
+        for (; r < n; ++r) if (sc.srow[r]) { if (q == 0) break; --q; }
+        sc.ssel[0] = r;
+      }
+      GroupSync<G>::sync();
+      sel_r = sc.ssel[0];
+      GroupSync<G>::sync();
+    }
+    rf.clear(sel_r);
+    if (tid == 0) sc.sperm[c] = sel_r;
+  }
+}
+
+// Goal for the general element types (int64 products or a non-integral
+// instance, sequential as _batch.py:192-197).  Returns the group total on
+// tid 0 (as raw bits for doubles).
+template <typename MT, int G, int CPL, typename Scratch>
+__device__ __noinline__ int64_t cost_general(const MT* cF, const MT* cD, int n, Scratch& sc,
+                                             int tid, int lane) {
+  constexpr int NT = 32 * G;
+  if constexpr (std::is_floating_point<MT>::value) {
+    double acc = 0.0;
+    if (tid == 0) {
+      acc = (double)cF[0] * (double)cD[0] * 0.0;
+      for (int i = 0; i < n; ++i) {
+        const int pi = sc.sperm[i];
+        for (int j = 0; j < n; ++j)
+          acc = __dadd_rn(acc, __dmul_rn((double)cF[i * n + j], (double)cD[pi * n + sc.sperm[j]]));
+      }
+    }
+    return __double_as_longlong(acc);
+  } else {
+    uint64_t part = 0;
+    for (int j = tid; j < n; j += NT) {
+      const int pj = sc.sperm[j];
+      for (int i = 0; i < n; ++i) {
+        if constexpr (sizeof(MT) <= 2)
+          part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj]);
+        else
+          part += (uint64_t)cF[i * n + j] * (uint64_t)cD[sc.sperm[i] * n + pj];
+      }
+    }
+    int64_t tot = warp_sum_i64((int64_t)part);
+    if constexpr (G > 1) {
+      __syncthreads();
+      if (lane == 0) sc.lslots[tid >> 5] = tot;
+      __syncthreads();
+      tot = 0;
+      for (int w = 0; w < G; ++w) tot += sc.lslots[w];
+    }
+    return tot;
+  }
+}
+
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 __global__ void __launch_bounds__(32 * G * W, (G == 1 ? QSB_MINB : 1))
@@ -286,7 +484,7 @@ step_kernel(const StepArgs a) {
   const int64_t ngroups = (int64_t)gridDim.x * W;
   const int row_w = 2 + 2 * n;
   uint32_t phase = 0;
-  int par = 0, ipar = 0;
+  int par = 0;
 
   for (int64_t p = (int64_t)blockIdx.x * W + gidx; p < a.P; p += ngroups) {
     VT* gV = reinterpret_cast<VT*>(a.V) + p * a.vstride;
@@ -337,121 +535,156 @@ step_kernel(const StepArgs a) {
     }
 
     // ================= phase 1: velocity update (_batch.py:39-50)
+    // Row-outer loops over the CPL owned columns: every column still sums in
+    // row order (the reference's order), and the lanes share loop overhead.
     VT total[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) total[k] = (VT)0;
     if (do_vel) {
+      if constexpr (sizeof(VT) == 8) {
+        // reference order, no contraction: (c1*v + c2r2*(pl-x)) + c3r3*(pg-x)
+        const double z2 = __dmul_rn(c2r2, 0.0), z3 = __dmul_rn(c3r3, 0.0);
+        double tot[CPL];
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        if (!cfree[k]) continue;
-        const int c = col[k];
-        const int xr = zr[k], lr = plr[k], gr = pgr[k];
-        if constexpr (sizeof(VT) == 8) {
-          // reference order, no contraction: (c1*v + c2r2*(pl-x)) + c3r3*(pg-x)
-          const double z2 = __dmul_rn(c2r2, 0.0), z3 = __dmul_rn(c3r3, 0.0);
-          double tot = 0.0;
-          for (int r = 0; r < n; ++r) {
-            const double v = (double)tile[r * n + c];
+        for (int k = 0; k < CPL; ++k) tot[k] = 0.0;
+        for (int r = 0; r < n; ++r) {
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            if (!cfree[k]) continue;
+            const int xr = zr[k], lr = plr[k], gr = pgr[k];
+            double* cell = tile + r * n + col[k];
+            const double v = *cell;
+            const bool special = r == xr || r == lr || r == gr;
             double lin;
-            if (r == xr || r == lr || r == gr) {
+            if (special) {
               const double d2 = (r == lr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
               const double d3 = (r == gr) ? ((r == xr) ? 0.0 : 1.0) : ((r == xr) ? -1.0 : 0.0);
               lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), __dmul_rn(c2r2, d2)), __dmul_rn(c3r3, d3));
             } else {
               lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), z2), z3);
             }
-            if (!a.v_bounded || r == xr || r == lr || r == gr) {
+            if (!a.v_bounded || special) {
               if (lin > a.vmax) lin = a.vmax;
               else if (lin < -a.vmax) lin = -a.vmax;
             }
-            tile[r * n + c] = (VT)lin;
-            tot = __dadd_rn(tot, fabs(lin));
+            *cell = lin;
+            tot[k] = __dadd_rn(tot[k], fabs(lin));
           }
-          total[k] = (VT)tot;
+        }
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) total[k] = (VT)tot[k];
+      } else {
+        // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
+        // x / pl / pg are patched afterwards (sum order is not significant
+        // under the fp32 tolerance)
+        const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
+        const float vm = (float)a.vmax;
+        float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          tot[k] = 0.f;
+          vx[k] = vl[k] = vg[k] = 0.f;
+          if (cfree[k]) {
+            vx[k] = tile[zr[k] * n + col[k]];
+            vl[k] = tile[plr[k] * n + col[k]];
+            vg[k] = tile[pgr[k] * n + col[k]];
+          }
+        }
+        if (a.v_bounded) {
+          // |c1 v| <= v_max is guaranteed for every stored v: no clamp
+#pragma unroll 2
+          for (int r = 0; r < n; ++r) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+              const float lin = c1f * *cell;
+              *cell = lin;
+              tot[k] += fabsf(lin);
+            }
+          }
         } else {
-          // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
-          // x / pl / pg are patched afterwards (sum order is not significant
-          // under the fp32 tolerance)
-          const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
-          const float vm = (float)a.vmax;
-          const float vx = tile[xr * n + c], vl = tile[lr * n + c], vg = tile[gr * n + c];
-          float tot = 0.f;
-          if (a.v_bounded) {
-            // |c1 v| <= v_max is guaranteed for every stored v: no clamp
-#pragma unroll 4
-            for (int r = 0; r < n; ++r) {
-              const float lin = c1f * (float)tile[r * n + c];
-              tile[r * n + c] = (VT)lin;
-              tot += fabsf(lin);
-            }
-          } else {
-#pragma unroll 4
-            for (int r = 0; r < n; ++r) {
-              const float lin = fminf(fmaxf(c1f * (float)tile[r * n + c], -vm), vm);
-              tile[r * n + c] = (VT)lin;
-              tot += fabsf(lin);
+#pragma unroll 2
+          for (int r = 0; r < n; ++r) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+              const float lin = fminf(fmaxf(c1f * *cell, -vm), vm);
+              *cell = lin;
+              tot[k] += fabsf(lin);
             }
           }
+        }
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!cfree[k]) continue;
+          const int xr = zr[k], lr = plr[k], gr = pgr[k];
+          float* colp = reinterpret_cast<float*>(tile) + col[k];
           auto fix = [&](int r, float v0) {
             const float d2 = (float)((r == lr) - (r == xr));
             const float d3 = (float)((r == gr) - (r == xr));
             const float g = fminf(fmaxf(c1f * v0, -vm), vm);
             const float sp = fminf(fmaxf(fmaf(c3f, d3, fmaf(c2f, d2, c1f * v0)), -vm), vm);
-            tile[r * n + c] = (VT)sp;
-            tot += fabsf(sp) - fabsf(g);
+            colp[r * n] = sp;
+            tot[k] += fabsf(sp) - fabsf(g);
           };
-          fix(xr, vx);
-          if (lr != xr) fix(lr, vl);
-          if (gr != xr && gr != lr) fix(gr, vg);
-          total[k] = (VT)tot;
+          fix(xr, vx[k]);
+          if (lr != xr) fix(lr, vl[k]);
+          if (gr != xr && gr != lr) fix(gr, vg[k]);
+          total[k] = (VT)tot[k];
         }
       }
     }
 
     // ================= normalisation (_batch.py:51-58) + initial statistics
+    // Per column: max / tie count / first row of v over the non-z rows
+    // (the z row is masked to -inf; stored values are finite) and the z key.
     VT nmax[CPL];
     int ncnt[CPL], nrow[CPL];
     uint64_t nk64[CPL], zkey[CPL];
-    bool zel[CPL];
+    bool zel[CPL], scale[CPL];
+    VT inv[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
-      nmax[k] = (VT)0; ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
-      if (!cfree[k]) continue;
-      const int c = col[k];
-      const bool scale = do_vel && a.normalize && total[k] > (VT)0;
-      VT inv = (VT)1;
-      if constexpr (sizeof(VT) == 4) inv = scale ? 1.0f / total[k] : 1.0f;
-      if (do_agg) {
-        // branchless max / tie count / first row over the non-z rows; the z
-        // row is masked to -inf (all stored values are finite)
-        const VT NINF = (VT)(-INFINITY);
-        const int zrk = zr[k];
-        VT cur = NINF, zv = (VT)0;
-        int cn = 0, cr = -1;
+      nmax[k] = (VT)(-INFINITY); ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
+      scale[k] = cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
+      inv[k] = (VT)1;
+      if constexpr (sizeof(VT) == 4) inv[k] = scale[k] ? 1.0f / total[k] : 1.0f;
+    }
+    auto rescale = [&](VT v, int k) -> VT {
+      if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
+      else return v * inv[k];
+    };
+    if (do_agg) {
+      const VT NINF = (VT)(-INFINITY);
 #pragma unroll 2
-        for (int r = 0; r < n; ++r) {
-          VT v = tile[r * n + c];
-          if (scale) {
-            if constexpr (sizeof(VT) == 8) v = __ddiv_rn(v, total[k]);
-            else v = v * inv;
-            tile[r * n + c] = v;
-          }
-          const bool isz = r == zrk;
-          zv = isz ? v : zv;
-          const VT w = isz ? NINF : v;
-          const bool gt = w > cur;
-          cn = gt ? 1 : cn + ((w == cur && !isz) ? 1 : 0);
-          cr = gt ? r : cr;
-          cur = gt ? w : cur;
+      for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!cfree[k]) continue;
+          VT* cell = tile + r * n + col[k];
+          VT v = *cell;
+          if (scale[k]) { v = rescale(v, k); *cell = v; }
+          const VT w = r == zr[k] ? NINF : v;
+          const bool gt = w > nmax[k];
+          // (a -inf == -inf tie before the first non-z row is reset by gt)
+          ncnt[k] = gt ? 1 : ncnt[k] + (w == nmax[k] ? 1 : 0);
+          nrow[k] = gt ? r : nrow[k];
+          nmax[k] = gt ? w : nmax[k];
         }
-        nmax[k] = cur; ncnt[k] = cn; nrow[k] = cr;
-        nk64[k] = cn ? nonz_key(cur) : 0;
-        zkey[k] = z_key(zv);
-      } else if (scale) {
-        for (int r = 0; r < n; ++r) {
-          if constexpr (sizeof(VT) == 8) tile[r * n + c] = __ddiv_rn(tile[r * n + c], total[k]);
-          else tile[r * n + c] = tile[r * n + c] * inv;
-        }
+      }
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        nk64[k] = ncnt[k] ? nonz_key(nmax[k]) : 0;
+        zkey[k] = z_key(tile[zr[k] * n + col[k]]);
+      }
+    } else {
+      for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+          if (scale[k]) tile[r * n + col[k]] = rescale(tile[r * n + col[k]], k);
       }
     }
     if (!GT && do_vel && store_v) {
@@ -464,19 +697,17 @@ step_kernel(const StepArgs a) {
 
     // ================= phase 2: aggregation S_x(X + V)
     if (do_agg) {
-      uint64_t rfree[NW];
+      RowSet<NW> rf;
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const int lo = w * 64;
-        rfree[w] = (n - lo >= 64) ? ~0ULL : (n > lo ? ((1ULL << (n - lo)) - 1) : 0ULL);
+        rf.w[w] = (n - lo >= 64) ? ~0ULL : (n > lo ? ((1ULL << (n - lo)) - 1) : 0ULL);
       }
-      auto row_is_free = [&](int r) -> bool { return (rfree[r >> 6] >> (r & 63)) & 1ULL; };
-      auto mval = [&](int r, int c, int zrc) -> uint64_t {
-        return okey(cell_m(tile[r * n + c], r == zrc));
-      };
       int cursor = a.agg_base;     // next aggregation draw (column in the draw row)
 
-      if (a.mode != MODE_PICK_COLUMN) {
+      if (a.mode == MODE_PICK_COLUMN) {
+        agg_pick_column<VT, G, NW>(tile, n, sc, rf, dr, cursor, tid, lane);
+      } else {
         bool restricted = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
         // cached per-column candidate: (key, tie count, first row) of the
         // column's best eligible cell; recomputed only when its parts change
@@ -499,79 +730,7 @@ step_kernel(const StepArgs a) {
           ck[k] = 0; cc[k] = 0; cr[k] = -1;
           if (cfree[k]) recompute(k);
         }
-
-        // G == 1: rescan (cooperatively, lanes = rows) every column whose
-        // non-z maximum left; the owner lane stores the new statistics
-        auto warp_rescans = [&](const bool (&need)[CPL]) {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              unsigned mask = __ballot_sync(FULL, need[k]);
-              while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int c = src + k * 32;
-                const int zc = __shfl_sync(FULL, zr[k], src);
-                if constexpr (sizeof(VT) == 4) {
-                  // fp32: one 32-bit key per cell, three warp reductions
-                  unsigned km = 0, kc = 0, kr = INT_MAX;
-#pragma unroll
-                  for (int j = 0; j < CPL; ++j) {
-                    const int r = lane + j * 32;
-                    if (r >= n || r == zc || !row_is_free(r)) continue;
-                    const unsigned key = okey32(__fadd_rn((float)tile[r * n + c], 0.0f));
-                    if (key > km) { km = key; kc = 1; kr = r; }
-                    else if (key == km) ++kc;
-                  }
-                  const unsigned M = __reduce_max_sync(FULL, km);
-                  const bool match = km == M && kc > 0;
-                  const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
-                  const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
-                  if (lane == src) {
-                    ncnt[k] = (int)tot;
-                    nrow[k] = tot ? (int)rr : -1;
-                    nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
-                    nk64[k] = tot ? nonz_key(nmax[k]) : 0;
-                    recompute(k);
-                  }
-                } else {
-                  Best rb = best_none();
-#pragma unroll
-                  for (int j = 0; j < CPL; ++j) {
-                    const int r = lane + j * 32;
-                    if (r >= n || r == zc || !row_is_free(r)) continue;
-                    const uint64_t key = nonz_key(tile[r * n + c]);
-                    if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
-                    else if (key == rb.key) ++rb.cnt;
-                  }
-                  const Best rr = warp_best(rb);
-                  if (lane == src) {
-                    ncnt[k] = rr.cnt;
-                    nrow[k] = rr.cnt ? rr.col : -1;
-                    nk64[k] = rr.cnt ? rr.key : 0;
-                    nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
-                    recompute(k);
-                  }
-                }
-              }
-            }
-        };
-        // bulk z-cell assignment bookkeeping (G == 1): keys of z cells placed
-        // in bulk steps, whose tie-draw count is settled lazily
-        int nbulk = 0;
-        auto settle_bulk = [&]() {
-          if (nbulk == 0) return;
-          int firsts = 0;
-          for (int i = lane; i < nbulk; i += 32) {
-            const uint64_t ki = sc.sbulk[i];
-            bool first = true;
-            for (int j = 0; j < i; ++j) if (sc.sbulk[j] == ki) { first = false; break; }
-            firsts += first;
-          }
-          const int distinct = (int)__reduce_add_sync(FULL, (unsigned)firsts);
-          cursor += nbulk - distinct;
-          nbulk = 0;
-          __syncwarp();
-        };
+        int nbulk = 0;     // z keys placed by bulk steps, tie draws not yet counted
 
         for (int rnd = 0; rnd < n; ++rnd) {
           if (restricted && rnd == a.depth) {
@@ -579,13 +738,18 @@ step_kernel(const StepArgs a) {
             restricted = false;
 #pragma unroll
             for (int k = 0; k < CPL; ++k)
-              if (cfree[k]) { zel[k] = row_is_free(zr[k]); recompute(k); }
+              if (cfree[k]) { zel[k] = rf.has(zr[k]); recompute(k); }
           }
+          bool need[CPL];
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) need[k] = false;
+          bool bulk = false;
+
           // ---- bulk step (unrestricted rounds, G == 1): every free z cell
           // whose m = 1 + v exceeds the largest free non-z cell is selected
-          // before any non-z cell, in some order that does not change the
-          // result; a group of g equal keys costs g - 1 tie draws.  Assign
-          // them all at once instead of one round each.
+          // before any non-z cell, in an order that does not change the
+          // result; a group of g equal keys costs g - 1 tie draws (counted
+          // lazily, only if a later round needs a draw).
           if constexpr (G == 1 && CPL <= 2) {
             if (!restricted) {
               uint64_t ml = 0;
@@ -623,75 +787,61 @@ step_kernel(const StepArgs a) {
                 const unsigned rl = __reduce_or_sync(FULL, (unsigned)rbits);
                 const unsigned rh = __reduce_or_sync(FULL, (unsigned)(rbits >> 32));
                 const uint64_t rmask = ((uint64_t)rh << 32) | rl;
-                rfree[0] &= ~rmask;
+                rf.w[0] &= ~rmask;
                 rnd += nq - 1;
-                if (rnd >= n - 1) break;
                 // non-z statistics whose maximum row may have left
-                bool need[CPL];
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) {
-                  need[k] = false;
                   if (!cfree[k] || !ncnt[k]) continue;
-                  if (ncnt[k] == 1 && nrow[k] >= 0) need[k] = (rmask >> nrow[k]) & 1ULL;
-                  else need[k] = true;
+                  need[k] = (ncnt[k] == 1 && nrow[k] >= 0) ? ((rmask >> nrow[k]) & 1ULL) : true;
                 }
-                warp_rescans(need);
-                continue;
+                bulk = true;
               }
             }
           }
-          // ---- lane-local best of the cached candidates, then the group's
-          Best loc;
-          loc.key = ck[0]; loc.cnt = cc[0]; loc.col = col[0]; loc.row = cr[0];
-#pragma unroll
-          for (int k = 1; k < CPL; ++k) {
-            if (ck[k] > loc.key) { loc.key = ck[k]; loc.cnt = cc[k]; loc.col = col[k]; loc.row = cr[k]; }
-            else if (ck[k] == loc.key) loc.cnt += cc[k];
-          }
-          if (loc.cnt == 0) { loc.key = 0; loc.col = INT_MAX; }
-          const Best b = group_best<G>(loc, sc, par, lane, tid);
 
-          int sel_r = -1, sel_c = -1;
-          if (b.cnt == 0) {
-            // every remaining cell is excluded (a 1x1 remainder): the
-            // reference falls back to the unrestricted set (_batch.py:118-132)
+          if (!bulk) {
+            // ---- one round: lane-local best of the cached candidates, then the group's
+            Best loc;
+            loc.key = ck[0]; loc.cnt = cc[0]; loc.col = col[0]; loc.row = cr[0];
 #pragma unroll
-            for (int w = 0; w < NW; ++w)
-              if (sel_r < 0 && rfree[w]) sel_r = w * 64 + __ffsll((long long)rfree[w]) - 1;
-            int mc = INT_MAX;
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) if (cfree[k]) mc = min(mc, col[k]);
-            sel_c = group_min_int<G>(mc, sc, ipar, lane, tid);
-          } else {
-            int pick = 0;
-            if (b.cnt > 1) {
-              if constexpr (G == 1) settle_bulk();
-              const double u = dr.at(cursor++);
-              const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
-              pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
+            for (int k = 1; k < CPL; ++k) {
+              if (ck[k] > loc.key) { loc.key = ck[k]; loc.cnt = cc[k]; loc.col = col[k]; loc.row = cr[k]; }
+              else if (ck[k] == loc.key) loc.cnt += cc[k];
             }
+            if (loc.cnt == 0) { loc.key = 0; loc.col = INT_MAX; }
+            const Best b = group_best<G>(loc, sc, par, lane, tid);
+
+            int sel_r, sel_c;
             if (b.cnt == 1 && b.row >= 0) {
               sel_r = b.row; sel_c = b.col;
+            } else if (b.cnt == 0) {
+              // every remaining cell is excluded (a 1x1 remainder): the
+              // reference falls back to the unrestricted set (_batch.py:118-132)
+              sel_r = rf.first();
+              int mc = INT_MAX;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) if (cfree[k]) mc = min(mc, col[k]);
+              sel_c = group_min_sync<G>(mc, sc, lane, tid);
             } else if (b.cnt == 1) {
               // unique maximum in column b.col whose first row is not tracked
               sel_c = b.col;
+              GroupSync<G>::sync();
 #pragma unroll
               for (int k = 0; k < CPL; ++k) if (col[k] == sel_c) sc.ssel[3] = zel[k];
-              Sync::sync();
-              const bool zok = sc.ssel[3];
-              const int zc = sc.szr[sel_c];
-              int found = INT_MAX;
-#pragma unroll
-              for (int j = 0; j < CPL; ++j) {
-                const int r = tid + j * NT;
-                if (r < n && row_is_free(r) && (r != zc || zok) && mval(r, sel_c, zc) == b.key)
-                  found = min(found, r);
-              }
-              sel_r = group_min_int<G>(found, sc, ipar, lane, tid);
-              Sync::sync();
+              GroupSync<G>::sync();
+              sel_r = first_row_scan<VT, G, CPL, NW>(tile, n, sc, rf, b.key, sel_c, sc.ssel[3] != 0,
+                                                     tid, lane);
             } else {
-              // ---- ties: the pick-th tied cell in row-major order
+              // ---- ties: one draw, the pick-th tied cell in row-major order
+              if constexpr (G == 1) {
+                if (nbulk) { cursor += nbulk - bulk_distinct(sc, nbulk, lane); nbulk = 0; }
+              }
+              const double u = dr.at(cursor++);
+              const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
+              const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
               bool fast = false;
+              sel_r = sel_c = -1;
               if constexpr (G == 1 && CPL <= 2) {
                 // each tied column holds one tied cell with a known row: the
                 // row set is a 64-bit mask; distinct rows => the pick-th set
@@ -719,80 +869,93 @@ step_kernel(const StepArgs a) {
                 }
               }
               if (!fast) {
+                GroupSync<G>::sync();
 #pragma unroll
                 for (int k = 0; k < CPL; ++k)
                   if (cc[k] && ck[k] == b.key) sc.stie[col[k]] = zel[k] ? 2 : 1;
-                Sync::sync();
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                  const int r = tid + j * NT;
-                  if (r >= n) continue;
-                  int cnt = 0;
-                  if (row_is_free(r)) {
-                    for (int c = 0; c < n; ++c) {
-                      const int tf = sc.stie[c];
-                      if (!tf) continue;
-                      const int zc = sc.szr[c];
-                      if (r == zc && tf != 2) continue;
-                      if (mval(r, c, zc) == b.key) ++cnt;
-                    }
-                  }
-                  sc.srow[r] = cnt;
-                }
-                Sync::sync();
-                if (tid == 0) {
-                  int r = 0, acc = 0;
-                  while (acc + sc.srow[r] <= pick) { acc += sc.srow[r]; ++r; }
-                  int q = pick - acc, cc2 = -1;
-                  for (int c = 0; c < n; ++c) {
-                    const int tf = sc.stie[c];
-                    if (!tf) continue;
-                    const int zc = sc.szr[c];
-                    if (r == zc && tf != 2) continue;
-                    if (mval(r, c, zc) == b.key) {
-                      if (q == 0) { cc2 = c; break; }
-                      --q;
-                    }
-                  }
-                  sc.ssel[0] = r; sc.ssel[1] = cc2;
-                }
-                Sync::sync();
+                tie_select_slow<VT, G, NW>(tile, n, sc, rf, b.key, pick, tid);
                 sel_r = sc.ssel[0]; sel_c = sc.ssel[1];
-#pragma unroll
-                for (int k = 0; k < CPL; ++k) if (cfree[k]) sc.stie[col[k]] = 0;
-                Sync::sync();
+                GroupSync<G>::sync();
               }
             }
-          }
 
-          // ---- retire row sel_r and column sel_c; update the statistics
-          rfree[sel_r >> 6] &= ~(1ULL << (sel_r & 63));
-          bool need[CPL];
+            // ---- retire row sel_r and column sel_c; update the statistics
+            rf.clear(sel_r);
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            need[k] = false;
-            if (!cfree[k]) continue;
-            if (col[k] == sel_c) {
-              cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
-              sc.sperm[sel_c] = sel_r;
-              continue;
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+              if (col[k] == sel_c) {
+                cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
+                sc.sperm[sel_c] = sel_r;
+                continue;
+              }
+              bool chg = false;
+              if (zr[k] == sel_r) {                     // this column's z cell left
+                chg = zel[k];
+                zel[k] = false;
+              } else if (ncnt[k] && tile[sel_r * n + col[k]] == nmax[k]) {
+                if (nrow[k] == sel_r) nrow[k] = -1;
+                need[k] = --ncnt[k] == 0;
+                chg = true;
+              }
+              if (chg) recompute(k);
             }
-            bool chg = false;
-            if (zr[k] == sel_r) {                     // this column's z cell left
-              chg = zel[k];
-              zel[k] = false;
-            } else if (ncnt[k] && tile[sel_r * n + col[k]] == nmax[k]) {
-              if (nrow[k] == sel_r) nrow[k] = -1;
-              need[k] = --ncnt[k] == 0;
-              chg = true;
-            }
-            if (chg) recompute(k);
           }
-          if (rnd == n - 1) break;
+          if (rnd >= n - 1) break;
 
           // ---- cooperative rescans of columns whose non-z maximum was retired
           if constexpr (G == 1) {
-            warp_rescans(need);
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              unsigned mask = __ballot_sync(FULL, need[k]);
+              while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int c = src + k * 32;
+                const int zc = __shfl_sync(FULL, zr[k], src);
+                if constexpr (sizeof(VT) == 4) {
+                  // fp32: one 32-bit key per cell, three warp reductions
+                  unsigned km = 0, kc = 0, kr = INT_MAX;
+#pragma unroll
+                  for (int j = 0; j < CPL; ++j) {
+                    const int r = lane + j * 32;
+                    if (r >= n || r == zc || !rf.has(r)) continue;
+                    const unsigned key = okey32(__fadd_rn((float)tile[r * n + c], 0.0f));
+                    if (key > km) { km = key; kc = 1; kr = r; }
+                    else if (key == km) ++kc;
+                  }
+                  const unsigned M = __reduce_max_sync(FULL, km);
+                  const bool match = km == M && kc > 0;
+                  const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
+                  const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
+                  if (lane == src) {
+                    ncnt[k] = (int)tot;
+                    nrow[k] = tot ? (int)rr : -1;
+                    nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
+                    nk64[k] = tot ? nonz_key(nmax[k]) : 0;
+                    recompute(k);
+                  }
+                } else {
+                  Best rb = best_none();
+#pragma unroll
+                  for (int j = 0; j < CPL; ++j) {
+                    const int r = lane + j * 32;
+                    if (r >= n || r == zc || !rf.has(r)) continue;
+                    const uint64_t key = nonz_key(tile[r * n + c]);
+                    if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
+                    else if (key == rb.key) ++rb.cnt;
+                  }
+                  const Best rr = warp_best(rb);
+                  if (lane == src) {
+                    ncnt[k] = rr.cnt;
+                    nrow[k] = rr.cnt ? rr.col : -1;
+                    nk64[k] = rr.cnt ? rr.key : 0;
+                    nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                    recompute(k);
+                  }
+                }
+              }
+            }
           } else {
             if (tid == 0) sc.ssel[2] = 0;
             __syncthreads();
@@ -808,7 +971,7 @@ step_kernel(const StepArgs a) {
 #pragma unroll
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
-                if (r >= n || r == zc || !row_is_free(r)) continue;
+                if (r >= n || r == zc || !rf.has(r)) continue;
                 const uint64_t key = nonz_key(tile[r * n + c]);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
@@ -827,58 +990,6 @@ step_kernel(const StepArgs a) {
             __syncthreads();
           }
         }
-      } else {
-        // ---------------- pick-column (_batch.py:78-88, 93-102, 145-153)
-        for (int i = tid; i < n; i += NT) sc.sorder[i] = i;
-        Sync::sync();
-        if (tid == 0) {
-          for (int i = n - 1; i > 0; --i) {
-            const double u = dr.at(cursor++);
-            long long j = (long long)__dmul_rn(u, (double)(i + 1));
-            if (j > i) j = i;
-            const int tmp = sc.sorder[i]; sc.sorder[i] = sc.sorder[j]; sc.sorder[j] = tmp;
-          }
-          sc.ssel[3] = cursor;
-        }
-        Sync::sync();
-        cursor = sc.ssel[3];
-        for (int rnd = 0; rnd < n; ++rnd) {
-          const int c = sc.sorder[rnd];
-          const int zc = sc.szr[c];
-          Best rb = best_none();
-#pragma unroll
-          for (int j = 0; j < CPL; ++j) {
-            const int r = tid + j * NT;
-            if (r >= n || !row_is_free(r)) continue;
-            const uint64_t key = mval(r, c, zc);
-            if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
-            else if (key == rb.key) ++rb.cnt;
-          }
-          const Best b = group_best<G>(rb, sc, par, lane, tid);
-          int sel_r = b.col;   // first matching row
-          if (b.cnt > 1) {
-            const double u = dr.at(cursor++);
-            const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
-            const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
-            // pick-th matching free row, ascending
-#pragma unroll
-            for (int j = 0; j < CPL; ++j) {
-              const int r = tid + j * NT;
-              if (r < n) sc.srow[r] = (row_is_free(r) && mval(r, c, zc) == b.key) ? 1 : 0;
-            }
-            Sync::sync();
-            if (tid == 0) {
-              int q = pick, r = 0;
-              for (; r < n; ++r) if (sc.srow[r]) { if (q == 0) break; --q; }
-              sc.ssel[0] = r;
-            }
-            Sync::sync();
-            sel_r = sc.ssel[0];
-            Sync::sync();
-          }
-          rfree[sel_r >> 6] &= ~(1ULL << (sel_r & 63));
-          if (tid == 0) sc.sperm[c] = sel_r;
-        }
       }
       Sync::sync();
       int16_t* gnew = a.perm_new + p * n;
@@ -887,41 +998,25 @@ step_kernel(const StepArgs a) {
 
     // ================= phase 3: goal  sum_ij F[i,j] * D[perm_i, perm_j]
     if (do_cost) {
-      if constexpr (kFloatMat) {
-        // non-integral instance: sequential i-major sum, as _batch.py:192-197
-        if (tid == 0) {
-          double acc = (double)cF[0] * (double)cD[0] * 0.0;
-          for (int i = 0; i < n; ++i) {
-            const int pi = sc.sperm[i];
-            for (int j = 0; j < n; ++j)
-              acc = __dadd_rn(acc, __dmul_rn((double)cF[i * n + j], (double)cD[pi * n + sc.sperm[j]]));
-          }
-          reinterpret_cast<double*>(a.cost)[p] = acc;
+      bool fast = false;
+      if constexpr (sizeof(MT) <= 2 && !kFloatMat) fast = a.acc32 != 0;
+      if (fast) {
+        // n * max(F) * max(D) < 2^32: per-column sums fit 32 bits; the row
+        // index perm[i] is loaded once for all owned columns
+        int pj[CPL];
+        uint32_t p32[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) { pj[k] = col[k] < n ? sc.sperm[col[k]] : 0; p32[k] = 0; }
+        for (int i = 0; i < n; ++i) {
+          const MT* Frow = cF + i * n;
+          const MT* Drow = cD + sc.sperm[i] * n;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            if (col[k] < n) p32[k] += (uint32_t)Frow[col[k]] * (uint32_t)Drow[pj[k]];
         }
-      } else {
         uint64_t part = 0;
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          const int j = col[k];
-          if (j >= n) continue;
-          const int pj = sc.sperm[j];
-          if constexpr (sizeof(MT) <= 2) {
-            if (a.acc32) {
-              // n * max(F) * max(D) < 2^32: the column sum fits 32 bits
-              uint32_t p32 = 0;
-#pragma unroll 4
-              for (int i = 0; i < n; ++i)
-                p32 += (uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj];
-              part += p32;
-            } else {
-              for (int i = 0; i < n; ++i)
-                part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj]);
-            }
-          } else {
-            for (int i = 0; i < n; ++i)
-              part += (uint64_t)cF[i * n + j] * (uint64_t)cD[sc.sperm[i] * n + pj];
-          }
-        }
+        for (int k = 0; k < CPL; ++k) part += p32[k];
         int64_t tot = warp_sum_i64((int64_t)part);
         if constexpr (G > 1) {
           if (lane == 0) sc.lslots[tid >> 5] = tot;
@@ -930,6 +1025,9 @@ step_kernel(const StepArgs a) {
           for (int w = 0; w < G; ++w) tot += sc.lslots[w];
         }
         if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;
+      } else {
+        const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane);
+        if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
       }
     }
 
