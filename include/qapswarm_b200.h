@@ -168,6 +168,17 @@ int qsb_step(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co
 /* Migration (migration.py:55-86) on the post-swap state. */
 int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream);
 
+/* 2-opt local search (north-star extension; no reference symbol, SURVEY.md
+ * 8a a11) on st->perm_new / st->cost, integral instances only.  Per pass the
+ * best pairwise facility exchange (smallest integer delta, ties to the
+ * lexicographically first (r, s)) is applied if it improves; at most
+ * `passes` moves.  QSB_TWOOPT_PBEST also performs the personal-best update
+ * (use it with qsb_step_phases without QSB_PHASE_PBEST). */
+#define QSB_TWOOPT_PBEST 1
+#define QSB_TWOOPT_SYMMETRIC 2   /* caller-checked: flow and distance symmetric, < 2^16 */
+int qsb_twoopt(const qsb_state* st, const qsb_instance* inst, int32_t passes, int32_t flags,
+               void* stream);
+
 /* Goal of P permutations (int16, device) -> out (int64 or f64, device). */
 int qsb_cost(const int16_t* perms, int64_t P, const qsb_instance* inst, void* out, void* stream);
 
@@ -202,6 +213,10 @@ int qsb_cost_many_i64(const int64_t* perms, const int64_t* flow, const int64_t* 
                       int64_t* out, int64_t P, int32_t n);
 int qsb_cost_many_f64(const int64_t* perms, const double* flow, const double* distance,
                       double* out, int64_t P, int32_t n);
+
+/* 2-opt on host buffers: perms (P, n) int64 and costs (P,) updated in place. */
+int qsb_twoopt_many(int64_t* perms, const int64_t* flow, const int64_t* distance, int64_t* costs,
+                    int64_t P, int32_t n, int32_t passes);
 
 /* streams.step_draws(seed, iteration, num_particles, n) (streams.py:53-64). */
 int qsb_step_draws_host(uint64_t seed, uint64_t t, int64_t P, int32_t n, double* out);

@@ -289,3 +289,39 @@ void orc_set_num_threads(int k) {
     (void)k;
 #endif
 }
+
+/* 2-opt (pairwise facility exchange) local search.  NOT in the reference
+ * (SPEC.md:148 lists delta evaluation as a non-goal):
+ * this is the north-star extension, and this function is its CPU oracle.
+ * Policy, per pass: evaluate every swap (r, s), r < s, with the exact
+ * integer delta; take the smallest delta, ties to
+ * the lexicographically first (r, s); apply it if it is negative, else stop.
+ * Costs use int64 wrap-around arithmetic like cost_many. */
+void orc_twoopt_many(int64_t *perms, const int64_t *F, const int64_t *D, int64_t *costs,
+                     int64_t P, int n, int passes) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < P; ++p) {
+        int64_t *pp = perms + p * n;
+        for (int pass = 0; pass < passes; ++pass) {
+            int64_t best = INT64_MAX;
+            int br = -1, bs = -1;
+            for (int r = 0; r < n; ++r) {
+                for (int s = r + 1; s < n; ++s) {
+                    const int64_t pr = pp[r], ps = pp[s];
+                    uint64_t d = (uint64_t)(F[r * n + r] - F[s * n + s]) * (uint64_t)(D[ps * n + ps] - D[pr * n + pr])
+                               + (uint64_t)(F[r * n + s] - F[s * n + r]) * (uint64_t)(D[ps * n + pr] - D[pr * n + ps]);
+                    for (int k = 0; k < n; ++k) {
+                        if (k == r || k == s) continue;
+                        const int64_t pk = pp[k];
+                        d += (uint64_t)(F[k * n + r] - F[k * n + s]) * (uint64_t)(D[pk * n + ps] - D[pk * n + pr])
+                           + (uint64_t)(F[r * n + k] - F[s * n + k]) * (uint64_t)(D[ps * n + pk] - D[pr * n + pk]);
+                    }
+                    if ((int64_t)d < best) { best = (int64_t)d; br = r; bs = s; }
+                }
+            }
+            if (br < 0 || best >= 0) break;
+            const int64_t t = pp[br]; pp[br] = pp[bs]; pp[bs] = t;
+            costs[p] = (int64_t)((uint64_t)costs[p] + (uint64_t)best);
+        }
+    }
+}

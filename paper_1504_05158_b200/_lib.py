@@ -20,6 +20,7 @@ QSB_OK, QSB_EINVAL, QSB_EUNSUPPORTED, QSB_ECUDA, QSB_EPERM = 0, 1, 2, 3, 4
 F32, F64, I64, U16 = 1, 2, 3, 4
 PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 4, 8, 16
 HINT_V_BOUNDED = 1
+TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V
 
 _vp = ctypes.c_void_p
@@ -75,6 +76,9 @@ SIGNATURES = {
                                 ctypes.POINTER(QsbCoeffs), _vp]),
     "qsb_migrate": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbMigration), _vp]),
     "qsb_cost": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(QsbInstance), _vp, _vp]),
+    "qsb_twoopt": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbInstance), _i32,
+                                  _i32, _vp]),
+    "qsb_twoopt_many": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32]),
     "qsb_step_draws": (ctypes.c_int, [_u64, _u64, _i64, _i64, _i32, _vp, _vp]),
     "qsb_init_population_device": (ctypes.c_int, [ctypes.POINTER(QsbState), _u64, _dbl, _vp]),
     "qsb_perm_to_matrix": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),

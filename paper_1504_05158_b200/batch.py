@@ -90,3 +90,15 @@ def step_draws(seed: int, iteration: int, num_particles: int, n: int) -> np.ndar
     _call("qsb_step_draws_host", int(seed) & (2**64 - 1), int(iteration), int(num_particles),
           int(n), out.ctypes.data)
     return out
+
+
+def twoopt_many(perms, flow, distance, costs, passes):
+    """2-opt extension (no reference symbol): in place on int64 perms (P, n)
+    and int64 costs (P,); integral instances only."""
+    perms = _c(perms, np.int64)
+    costs = _c(costs, np.int64)
+    P, n = perms.shape
+    f = np.ascontiguousarray(flow, dtype=np.int64)
+    d = np.ascontiguousarray(distance, dtype=np.int64)
+    _call("qsb_twoopt_many", perms.ctypes.data, f.ctypes.data, d.ctypes.data, costs.ctypes.data,
+          P, n, int(passes))

@@ -9,6 +9,9 @@ reference behaviour:
   (1 = every iteration, the reference; the north-star runs use 10);
 * ``precision`` -- ``"fp64"`` keeps the velocity state in float64 and is
   bit-identical to the reference; ``"fp32"`` is the throughput mode;
+* ``two_opt_passes`` -- after S_x, apply up to this many best-improvement
+  pairwise-exchange moves per particle (0 = off, the reference; the
+  north-star's 2-opt local search, integral instances only);
 * ``init`` -- ``"reference"`` draws the initial population from the
   reference's numpy init stream on the host (bit-identical); ``"device"``
   draws it on the GPU from a documented Philox stream (not the reference's).
@@ -73,6 +76,7 @@ class SolverConfig:
     migration_period: int = 1
     precision: str = "fp64"
     init: str = "reference"
+    two_opt_passes: int = 0
 
     def __post_init__(self):
         if self.swarms < 1 or self.swarm_size < 1:
@@ -92,6 +96,8 @@ class SolverConfig:
             raise ValueError("migration_period must be positive")
         if self.precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}, got {self.precision!r}")
+        if self.two_opt_passes < 0:
+            raise ValueError("two_opt_passes must be non-negative")
         if self.init not in INITS:
             raise ValueError(f"init must be one of {INITS}, got {self.init!r}")
 

@@ -8,6 +8,7 @@
 #include "../../include/qapswarm_b200.h"
 #include "aux_kernels.cuh"
 #include "step_kernel.cuh"
+#include "twoopt.cuh"
 
 using namespace qsb;
 
@@ -116,6 +117,36 @@ static int32_t vstride_of(int32_t n, int32_t v_dtype) {
   const int32_t per16 = v_dtype == QSB_F64 ? 2 : 4;
   const int32_t nn = n * n;
   return (nn + per16 - 1) / per16 * per16;
+}
+
+// 2-opt on the state's perm_new / cost (north-star extension, twoopt.cuh)
+template <typename MT, int NT>
+static int launch_twoopt(TwoOptArgs t, cudaStream_t s) {
+  using DT = MT;
+  const size_t nn = (size_t)t.n * t.n;
+  const size_t base = align_up(nn * sizeof(DT), 16) + align_up((size_t)t.n * 4, 16) + (NT / 32) * 12 + 64;
+  size_t smem = base + align_up(nn * sizeof(MT), 16);
+  t.f_smem = 1;
+  if (smem > smem_optin()) { smem = base; t.f_smem = 0; }
+  if (smem > smem_optin()) return QSB_EUNSUPPORTED;
+  auto fn = twoopt_kernel<MT, NT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  int bps = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, NT, smem);
+  if (bps < 1) bps = 1;
+  const int64_t cap = (int64_t)num_sms() * bps;
+  const int grid = (int)(t.P < cap ? t.P : cap);
+  if (grid <= 0) return QSB_OK;
+  fn<<<grid, NT, smem, s>>>(t);
+  return launch_status();
+}
+
+template <typename MT>
+static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s) {
+  return t.n <= 64 ? launch_twoopt<MT, 128>(t, s) : launch_twoopt<MT, 256>(t, s);
 }
 
 extern "C" {
@@ -333,6 +364,29 @@ int qsb_perm_to_matrix(const int16_t* perm, int64_t P, int32_t n, int8_t* x, voi
   return launch_status();
 }
 
+int qsb_twoopt(const qsb_state* st, const qsb_instance* inst, int32_t passes, int32_t flags,
+               void* stream) {
+  if (!st || !inst || st->n < 2 || inst->n != st->n || passes < 0) return QSB_EINVAL;
+  if (st->cost_dtype != QSB_I64 || inst->mat_dtype == QSB_F64) return QSB_EINVAL;
+  TwoOptArgs t{};
+  t.n = st->n;
+  t.P = st->num_particles;
+  t.passes = passes;
+  t.sym = (flags & QSB_TWOOPT_SYMMETRIC) ? 1 : 0;
+  t.do_pbest = (flags & QSB_TWOOPT_PBEST) ? 1 : 0;
+  t.perm = st->perm_new;
+  t.cost = (int64_t*)st->cost;
+  t.pl_perm = st->pl_perm;
+  t.pl_cost = (int64_t*)st->pl_cost;
+  t.improved = st->improved;
+  t.F = inst->flow;
+  t.D = inst->distance;
+  if (t.P == 0 || (passes == 0 && !t.do_pbest)) return QSB_OK;
+  if (t.do_pbest && (!t.pl_perm || !t.pl_cost || !t.improved)) return QSB_EINVAL;
+  if (inst->mat_dtype == QSB_U16) return dispatch_twoopt<uint16_t>(t, (cudaStream_t)stream);
+  return dispatch_twoopt<int64_t>(t, (cudaStream_t)stream);
+}
+
 }  // extern "C"
 
 // ------------------------------------------------- tier 1: host buffers
@@ -536,4 +590,54 @@ int qsb_step_draws_host(uint64_t seed, uint64_t t, int64_t P, int32_t n, double*
   return QSB_OK;
 }
 
+int qsb_twoopt_many(int64_t* perms, const int64_t* flow, const int64_t* distance, int64_t* costs,
+                    int64_t P, int32_t n, int32_t passes) {
+  if (!perms || !flow || !distance || !costs || n < 2 || P < 0 || passes < 0) return QSB_EINVAL;
+  if (P == 0) return QSB_OK;
+  HostCtx& h = hctx();
+  std::lock_guard<std::mutex> lock(h.mu);
+  QSB_TRY(h.init());
+  const int64_t nn = (int64_t)n * n;
+  cudaStream_t s = h.stream;
+  // symmetric instances use the halved delta sweep (exact: products < 2^63)
+  bool sym = true;
+  for (int i = 0; i < n && sym; ++i)
+    for (int j = 0; j < i; ++j)
+      if (flow[i * n + j] != flow[j * n + i] || distance[i * n + j] != distance[j * n + i]) { sym = false; break; }
+  int64_t mx = 0;
+  for (int64_t i = 0; i < nn; ++i) { if (flow[i] > mx) mx = flow[i]; if (distance[i] > mx) mx = distance[i]; }
+  if (mx >= (1 << 16)) sym = false;
+  QSB_TRY(h.b[6].ensure(P * n * 2 + P * 8 + 16));
+  QSB_TRY(h.b[7].ensure(2 * nn * 8));
+  const bool narrow = mx < (1 << 16);   // uint16 device matrices when exact
+  int16_t* dp = (int16_t*)h.b[6].p;
+  int64_t* dc = (int64_t*)((char*)h.b[6].p + align_up(P * n * 2, 16));
+  std::vector<int16_t> hp((size_t)(P * n));
+  for (int64_t i = 0; i < P * n; ++i) hp[(size_t)i] = (int16_t)perms[i];
+  QSB_CUDA(cudaMemcpyAsync(dp, hp.data(), P * n * 2, cudaMemcpyHostToDevice, s));
+  QSB_CUDA(cudaMemcpyAsync(dc, costs, P * 8, cudaMemcpyHostToDevice, s));
+  std::vector<uint16_t> narrow_fd;
+  if (narrow) {
+    narrow_fd.resize((size_t)(2 * nn));
+    for (int64_t i = 0; i < nn; ++i) { narrow_fd[(size_t)i] = (uint16_t)flow[i]; narrow_fd[(size_t)(nn + i)] = (uint16_t)distance[i]; }
+    QSB_CUDA(cudaMemcpyAsync(h.b[7].p, narrow_fd.data(), 2 * nn * 2, cudaMemcpyHostToDevice, s));
+  } else {
+    QSB_CUDA(cudaMemcpyAsync(h.b[7].p, flow, nn * 8, cudaMemcpyHostToDevice, s));
+    QSB_CUDA(cudaMemcpyAsync((char*)h.b[7].p + nn * 8, distance, nn * 8, cudaMemcpyHostToDevice, s));
+  }
+  TwoOptArgs t{};
+  t.n = n; t.P = P; t.passes = passes; t.sym = sym ? 1 : 0; t.do_pbest = 0;
+  t.perm = dp; t.cost = dc;
+  t.F = h.b[7].p;
+  t.D = (char*)h.b[7].p + nn * (narrow ? 2 : 8);
+  if (narrow) QSB_TRY(dispatch_twoopt<uint16_t>(t, s));
+  else QSB_TRY(dispatch_twoopt<int64_t>(t, s));
+  QSB_CUDA(cudaMemcpyAsync(hp.data(), dp, P * n * 2, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaMemcpyAsync(costs, dc, P * 8, cudaMemcpyDeviceToHost, s));
+  QSB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < P * n; ++i) perms[i] = hp[(size_t)i];
+  return QSB_OK;
+}
+
 }  // extern "C"
+

@@ -1,0 +1,154 @@
+// twoopt.cuh -- 2-opt (pairwise facility exchange) local search, integer.
+//
+// Not part of the reference (the reference lists delta
+// evaluation as a non-goal).  North-star extension, applied to
+// each particle's new permutation after S_x and the goal, before the personal
+// best.  Policy per pass: evaluate every swap (r, s), r < s, with the exact
+// integer delta of SURVEY.md Appendix A4, take the smallest delta with ties
+// to the lexicographically first (r, s), apply it if negative, else stop.
+// CPU oracle: orc_twoopt_many in oracle/qap_oracle.c.
+//
+// One CTA per particle.  The permuted distance matrix Dp[i][j] = D[p_i][p_j]
+// lives in shared memory, so a delta is a contiguous O(n) sweep; a move
+// swaps two rows and two columns of Dp.  All n(n-1)/2 deltas of a pass are
+// scored in parallel (pair q -> (r, s) by closed-form unranking) and reduced
+// to the lexicographic (delta, q) minimum.
+#pragma once
+#include <type_traits>
+#include "common.cuh"
+
+namespace qsb {
+
+struct TwoOptArgs {
+  int n;
+  int64_t P;
+  int passes;
+  int sym;          // F and D symmetric (halves the delta sweep)
+  int do_pbest;     // also apply the personal-best update (engine.py:211-215)
+  int f_smem;       // F staged in shared memory
+  int16_t* perm;    // (P, n) in/out: the particles' new positions
+  int64_t* cost;    // (P,) in/out
+  int16_t* pl_perm;
+  int64_t* pl_cost;
+  uint8_t* improved;
+  const void* F;
+  const void* D;
+};
+
+__device__ __forceinline__ void unrank_pair(int64_t q, int n, int& r, int& s) {
+  const double t = sqrt((double)(-8 * q + 4 * (int64_t)n * (n - 1) - 7));
+  r = n - 2 - (int)floor(t / 2.0 - 0.5);
+  s = (int)(q + r + 1 - (int64_t)n * (n - 1) / 2 + (int64_t)(n - r) * (n - r - 1) / 2);
+}
+
+template <typename MT, int NT>
+__global__ void __launch_bounds__(NT) twoopt_kernel(const TwoOptArgs a) {
+  using DT = MT;   // Dp holds D entries, same range
+  extern __shared__ __align__(16) unsigned char tsm[];
+  const int n = a.n;
+  const int nn = n * n;
+  DT* Dp = reinterpret_cast<DT*>(tsm);
+  size_t off = align_up((size_t)nn * sizeof(DT), 16);
+  MT* sF = reinterpret_cast<MT*>(tsm + off);
+  if (a.f_smem) off += align_up((size_t)nn * sizeof(MT), 16);
+  int* sp = reinterpret_cast<int*>(tsm + off);
+  off += align_up((size_t)n * sizeof(int), 16);
+  int64_t* rd = reinterpret_cast<int64_t*>(tsm + off);
+  int* rq = reinterpret_cast<int*>(rd + NT / 32);
+  __shared__ int s_move;
+
+  const MT* gF = reinterpret_cast<const MT*>(a.F);
+  const MT* gD = reinterpret_cast<const MT*>(a.D);
+  if (a.f_smem)
+    for (int i = threadIdx.x; i < nn; i += NT) sF[i] = gF[i];
+  const MT* F = a.f_smem ? sF : gF;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t npairs = (int64_t)n * (n - 1) / 2;
+
+  for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) sp[i] = a.perm[p * n + i];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nn; e += NT) Dp[e] = (DT)gD[sp[e / n] * n + sp[e % n]];
+    __syncthreads();
+    uint64_t cost = (uint64_t)a.cost[p];
+    for (int pass = 0; pass < a.passes; ++pass) {
+      int64_t best = INT64_MAX;
+      int bq = INT_MAX;
+      for (int64_t q = threadIdx.x; q < npairs; q += NT) {
+        int r, s;
+        unrank_pair(q, n, r, s);
+        const DT* Dr = Dp + r * n;
+        const DT* Ds = Dp + s * n;
+        uint64_t d = (uint64_t)((int64_t)F[r * n + r] - F[s * n + s]) * (uint64_t)((int64_t)Ds[s] - Dr[r]);
+        uint64_t acc = 0;
+        if (a.sym) {
+          // F, D symmetric: both k-terms are equal and the (r,s) cross term vanishes
+          for (int k = 0; k < n; ++k) {
+            if (k == r || k == s) continue;
+            acc += (uint64_t)((int64_t)F[k * n + r] - F[k * n + s]) * (uint64_t)((int64_t)Ds[k] - Dr[k]);
+          }
+          d += 2 * acc;
+        } else {
+          d += (uint64_t)((int64_t)F[r * n + s] - F[s * n + r]) * (uint64_t)((int64_t)Ds[r] - Dr[s]);
+          for (int k = 0; k < n; ++k) {
+            if (k == r || k == s) continue;
+            const DT* Dk = Dp + k * n;
+            acc += (uint64_t)((int64_t)F[k * n + r] - F[k * n + s]) * (uint64_t)((int64_t)Dk[s] - Dk[r])
+                 + (uint64_t)((int64_t)F[r * n + k] - F[s * n + k]) * (uint64_t)((int64_t)Ds[k] - Dr[k]);
+          }
+          d += acc;
+        }
+        const int64_t dd = (int64_t)d;
+        if (dd < best) { best = dd; bq = (int)q; }   // q ascends per thread: first wins
+      }
+      // lexicographic (delta, q) minimum over the CTA
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      if (lane == 0) { rd[warp] = best; rq[warp] = bq; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < NT / 32; ++w)
+          if (rd[w] < rd[0] || (rd[w] == rd[0] && rq[w] < rq[0])) { rd[0] = rd[w]; rq[0] = rq[w]; }
+        s_move = (rq[0] != INT_MAX && rd[0] < 0) ? rq[0] : -1;
+      }
+      __syncthreads();
+      const int mq = s_move;
+      if (mq < 0) break;
+      cost += (uint64_t)rd[0];
+      int r, s;
+      unrank_pair(mq, n, r, s);
+      // swap facilities r and s: rows r, s then columns r, s of Dp
+      for (int j = threadIdx.x; j < n; j += NT) {
+        const DT t = Dp[r * n + j]; Dp[r * n + j] = Dp[s * n + j]; Dp[s * n + j] = t;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += NT) {
+        const DT t = Dp[i * n + r]; Dp[i * n + r] = Dp[i * n + s]; Dp[i * n + s] = t;
+      }
+      if (threadIdx.x == 0) { const int t = sp[r]; sp[r] = sp[s]; sp[s] = t; }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += NT) a.perm[p * n + i] = (int16_t)sp[i];
+    if (a.do_pbest) {
+      // one thread decides (strict <, engine.py:211), then all copy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const bool imp = (int64_t)cost < a.pl_cost[p];
+        if (imp) a.pl_cost[p] = (int64_t)cost;
+        a.improved[p] = imp ? 1 : 0;
+        s_move = imp;
+      }
+      __syncthreads();
+      if (s_move)
+        for (int i = threadIdx.x; i < n; i += NT) a.pl_perm[p * n + i] = (int16_t)sp[i];
+    }
+    if (threadIdx.x == 0) a.cost[p] = (int64_t)cost;
+  }
+}
+
+}  // namespace qsb

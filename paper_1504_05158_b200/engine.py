@@ -273,6 +273,8 @@ class _Runtime:
         self.inst = _lib.QsbInstance(state.n, code, self.flow.data_ptr(), self.dist.data_ptr(),
                                      acc32, 0)
         self.mat_code = code
+        fa, da = np.asarray(instance.flow), np.asarray(instance.distance)
+        self.symmetric = bool(code == _lib.U16 and (fa == fa.T).all() and (da == da.T).all())
         self.key = (id(instance), config.coefficients, config.seed)
         c = config.coefficients
         self.coeffs = _lib.QsbCoeffs(c.c1, c.c2, c.c3, c.v_max, int(c.sv_mode == "norm"),
@@ -455,12 +457,19 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     cs = state.c_state()
     # |c1 v| <= v_max for every stored v => the bulk-row clamp is a no-op
     rt.coeffs.hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
+    passes = config.two_opt_passes
+    if passes and not state.integral:
+        raise ValueError("two_opt_passes requires an integral instance")
+    flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
     if timer is not None:
         timer.before(stream)
-    _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, _lib.PHASE_ALL, None, 0, 2, None, 0,
-              stream)
+    _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, flags, None, 0, 2, None, 0, stream)
     if timer is not None:
         timer.after(stream)
+    if passes:
+        tf = _lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+        _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, stream)
+        state.launches += 1
     _lib.call("qsb_best_update", cs, stream)
     state.launches += 2
     # after S_v every entry is clamped to v_max, or normalised to |v| <= 1

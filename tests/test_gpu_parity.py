@@ -253,3 +253,49 @@ def test_north_star_shape_properties():
     assert np.array_equal(c, st.cost[sample])
     assert st.best_cost == orc.evaluate_cost(inst.flow, inst.distance, st.best_perm)
     assert len(st.migration_log) == int(0.33 * 800)
+
+
+# ------------------------------------------------------------------ 2-opt
+@pytest.mark.parametrize("n,sym", [(12, True), (30, True), (30, False), (64, False),
+                                   (65, True), (100, False), (200, True)])
+@pytest.mark.parametrize("passes", [1, 4])
+def test_twoopt_many_vs_oracle(n, sym, passes):
+    rng = np.random.default_rng(n * 10 + passes)
+    f = rng.integers(0, 100, (n, n))
+    d = rng.integers(0, 100, (n, n))
+    if sym:
+        f = np.triu(f, 1) + np.triu(f, 1).T
+        d = np.triu(d, 1) + np.triu(d, 1).T
+    perms = np.array([rng.permutation(n) for _ in range(37)], dtype=np.int64)
+    costs = np.zeros(37, np.int64)
+    orc.cost_many(perms, f, d, costs)
+    a_p, a_c = perms.copy(), costs.copy()
+    b_p, b_c = perms.copy(), costs.copy()
+    orc.twoopt_many(a_p, f, d, a_c, passes)
+    batch.twoopt_many(b_p, f, d, b_c, passes)
+    assert np.array_equal(a_p, b_p)
+    assert np.array_equal(a_c, b_c)
+
+
+@pytest.mark.parametrize("passes,precision", [(1, "fp64"), (3, "fp64"), (2, "fp32")])
+def test_step_with_twoopt_matches_oracle(passes, precision, golden_instances):
+    """Config-2 shape (n=30, independent swarms, 2-opt on), scaled down."""
+    inst = golden_instances["tai30"]
+    cfg = qsb.SolverConfig(swarms=5, swarm_size=20, seed=4, two_opt_passes=passes,
+                           precision=precision,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    st = qsb.init_population(cfg, inst)
+    ost = orc.init_population(5, 20, inst.n, inst.flow, inst.distance, seed=4)
+    kw = orc.coeff_kwargs(cfg)
+    for _ in range(6):
+        if precision == "fp32":
+            ost.V = st.V.astype(np.float64)   # replay the GPU's own velocities
+        qsb.step(st, inst, cfg)
+        orc.step(ost, inst.flow, inst.distance, **kw)
+        if precision == "fp64":
+            assert st.V.tobytes() == ost.V.tobytes()
+        assert np.array_equal(st.perms, ost.perms)
+        assert np.array_equal(st.cost, ost.cost)
+        assert np.array_equal(st.pl_cost, ost.pl_cost)
+        assert np.array_equal(st.bests.costs, ost.pg_costs)
+        assert st.best_cost == ost.best_cost

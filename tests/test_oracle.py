@@ -138,3 +138,39 @@ def test_trajectory_golden(name, trajectories, golden_instances):
         assert [st.best_cost, st.best_iteration] == tr["bests"][t + 1]
     assert st.best_perm.tolist() == tr["best_perm"]
     assert [list(e) for e in st.migration_log] == tr["migration_log"]
+
+
+def test_twoopt_oracle_against_bruteforce(golden_instances):
+    """2-opt has no reference symbol: its oracle is pinned by brute force --
+    every applied move is the best (lexicographically first) exchange and
+    the costs equal evaluate_cost."""
+    rng = np.random.default_rng(3)
+    for name in ("chr12a", "tai30"):
+        inst = golden_instances[name]
+        n = inst.n
+        perms = np.array([rng.permutation(n) for _ in range(6)], dtype=np.int64)
+        costs = np.zeros(6, np.int64)
+        orc.cost_many(perms, inst.flow, inst.distance, costs)
+        for p in range(6):
+            q = perms[p:p + 1].copy()
+            c = costs[p:p + 1].copy()
+            orc.twoopt_many(q, inst.flow, inst.distance, c, 1)
+            base = orc.evaluate_cost(inst.flow, inst.distance, perms[p])
+            best, arg = 0, None
+            for r in range(n):
+                for s in range(r + 1, n):
+                    t = perms[p].copy()
+                    t[r], t[s] = t[s], t[r]
+                    dlt = orc.evaluate_cost(inst.flow, inst.distance, t) - base
+                    if dlt < best:
+                        best, arg = dlt, t
+            expect = arg if arg is not None else perms[p]
+            assert np.array_equal(q[0], expect)
+            assert c[0] == orc.evaluate_cost(inst.flow, inst.distance, q[0])
+        # many passes never increase the cost and stay consistent
+        q = perms.copy()
+        c = costs.copy()
+        orc.twoopt_many(q, inst.flow, inst.distance, c, 50)
+        assert (c <= costs).all()
+        for p in range(6):
+            assert c[p] == orc.evaluate_cost(inst.flow, inst.distance, q[p])
