@@ -155,6 +155,7 @@ struct GroupScratch {
   int sorder[NMAX];    // pick-column visiting order
   unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
   uint64_t sbulk[NMAX];      // z keys assigned by bulk steps (pending tie-draw count)
+  uint64_t tmask[NMAX];      // per tied column: mask of tied rows (one-warp tie path)
   Best slots[2][G];
   int islots[2][G];
   int64_t lslots[G];
@@ -322,17 +323,86 @@ __device__ __noinline__ int first_row_scan(const VT* tile, int n, Scratch& sc, R
   return group_min_sync<G>(found, sc, lane, tid);
 }
 
-// Number of distinct keys among the z cells placed by bulk steps.
+// Number of distinct keys among the z cells placed by bulk steps (n <= 64:
+// two list entries per lane, match.any within each half, a short loop for
+// values shared across the halves).
 template <typename Scratch>
 __device__ __noinline__ int bulk_distinct(const Scratch& sc, int nb, int lane) {
-  int firsts = 0;
-  for (int i = lane; i < nb; i += 32) {
-    const uint64_t ki = sc.sbulk[i];
-    bool first = true;
-    for (int j = 0; j < i; ++j) if (sc.sbulk[j] == ki) { first = false; break; }
-    firsts += first;
+  const bool v0 = lane < nb, v1 = lane + 32 < nb;
+  const unsigned long long e0 = v0 ? sc.sbulk[lane] : 0ULL;
+  const unsigned long long e1 = v1 ? sc.sbulk[lane + 32] : 0ULL;
+  const unsigned m0 = __match_any_sync(FULL, e0);
+  const unsigned m1 = __match_any_sync(FULL, e1);
+  const bool f0 = v0 && (__ffs(m0) - 1) == lane;
+  const bool f1 = v1 && (__ffs(m1) - 1) == lane;
+  int distinct = __popc(__ballot_sync(FULL, f0));
+  unsigned firsts1 = __ballot_sync(FULL, f1);
+  while (firsts1) {
+    const int src = __ffs(firsts1) - 1;
+    firsts1 &= firsts1 - 1;
+    const unsigned long long v = __shfl_sync(FULL, e1, src);
+    distinct += __any_sync(FULL, v0 && e0 == v) ? 0 : 1;
   }
-  return (int)__reduce_add_sync(FULL, (unsigned)firsts);
+  return distinct;
+}
+
+// Tie round for one-warp groups (n <= 64): the pick-th tied cell in
+// row-major order (_batch.py:155-170).  Owners have flagged the tied columns
+// in sc.stie (2 = its z cell is eligible).  Each tied column contributes a
+// 64-bit mask of tied rows; a warp prefix sum over per-row counts finds the
+// row, and the pick-th tied column of that row (ascending) the cell.
+// Returns (row << 8) | col; clears the flags.
+template <typename VT, typename Scratch>
+__device__ __noinline__ int tie_select_warp(const VT* tile, int n, Scratch& sc, uint64_t rfree,
+                                            uint64_t key, int pick, int lane) {
+  __syncwarp();
+  const int c0 = lane, c1 = lane + 32;
+  const bool t0 = sc.stie[c0] != 0;
+  const bool t1 = c1 < n && sc.stie[c1] != 0;
+  unsigned tb[2] = {__ballot_sync(FULL, t0), __ballot_sync(FULL, t1)};
+  int cnt0 = 0, cnt1 = 0;
+  const bool r0ok = c0 < n && ((rfree >> c0) & 1ULL);
+  const bool r1ok = c1 < n && ((rfree >> c1) & 1ULL);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    unsigned b = tb[h];
+    while (b) {
+      const int c = h * 32 + __ffs(b) - 1;
+      b &= b - 1;
+      const int zc = sc.szr[c];
+      const bool zok = sc.stie[c] == 2;
+      const bool a0 = r0ok && (c0 != zc || zok) && mkey(tile, n, c0, c, zc) == key;
+      const bool a1 = r1ok && (c1 != zc || zok) && mkey(tile, n, c1, c, zc) == key;
+      const unsigned m0 = __ballot_sync(FULL, a0), m1 = __ballot_sync(FULL, a1);
+      cnt0 += a0;
+      cnt1 += a1;
+      if (lane == 0) sc.tmask[c] = ((uint64_t)m1 << 32) | m0;
+    }
+  }
+  // inclusive prefix of the per-row counts, rows 0..31 then 32..63
+  int p0 = cnt0, p1 = cnt1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u0 = __shfl_up_sync(FULL, p0, o), u1 = __shfl_up_sync(FULL, p1, o);
+    if (lane >= o) { p0 += u0; p1 += u1; }
+  }
+  const int tot0 = __shfl_sync(FULL, p0, 31);
+  p1 += tot0;
+  const unsigned h0 = __ballot_sync(FULL, cnt0 && p0 - cnt0 <= pick && pick < p0);
+  const unsigned h1 = __ballot_sync(FULL, cnt1 && p1 - cnt1 <= pick && pick < p1);
+  int row, q;
+  if (h0) { row = __ffs(h0) - 1; q = pick - (__shfl_sync(FULL, p0 - cnt0, row)); }
+  else { const int l = __ffs(h1) - 1; row = 32 + l; q = pick - (__shfl_sync(FULL, p1 - cnt1, l)); }
+  __syncwarp();
+  const bool b0 = t0 && ((sc.tmask[c0] >> row) & 1ULL);
+  const bool b1 = t1 && ((sc.tmask[c1] >> row) & 1ULL);
+  const unsigned w0 = __ballot_sync(FULL, b0), w1 = __ballot_sync(FULL, b1);
+  const int n0 = __popc(w0);
+  const int col = q < n0 ? nth_set_bit32(w0, q) : 32 + nth_set_bit32(w1, q - n0);
+  if (t0) sc.stie[c0] = 0;
+  if (t1) sc.stie[c1] = 0;
+  __syncwarp();
+  return (row << 8) | col;
 }
 
 // pick-column S_x (_batch.py:78-88, 93-102, 145-153): Fisher-Yates column
@@ -843,9 +913,9 @@ step_kernel(const StepArgs a) {
               bool fast = false;
               sel_r = sel_c = -1;
               if constexpr (G == 1 && CPL <= 2) {
-                // each tied column holds one tied cell with a known row: the
-                // row set is a 64-bit mask; distinct rows => the pick-th set
-                // bit is the answer (the common case: x cells tied at 1 + 0)
+                // common case: each tied column holds one tied cell with a
+                // known row -> the row set is a 64-bit mask and the pick-th
+                // set bit is the answer (e.g. x cells tied at 1 + 0)
                 bool slow = false;
                 uint64_t rm = 0;
 #pragma unroll
@@ -865,8 +935,16 @@ step_kernel(const StepArgs a) {
                   for (int k = 0; k < CPL; ++k)
                     owner[k] = __ballot_sync(FULL, cc[k] && ck[k] == b.key && cr[k] == sel_r);
                   sel_c = owner[0] ? __ffs(owner[0]) - 1 : 32 + __ffs(owner[CPL - 1]) - 1;
-                  fast = true;
+                } else {
+                  // general ties: per-column row masks + warp prefix over rows
+#pragma unroll
+                  for (int k = 0; k < CPL; ++k)
+                    if (cc[k] && ck[k] == b.key) sc.stie[col[k]] = zel[k] ? 2 : 1;
+                  const int rc = tie_select_warp<VT>(tile, n, sc, rf.w[0], b.key, pick, lane);
+                  sel_r = rc >> 8;
+                  sel_c = rc & 0xff;
                 }
+                fast = true;
               }
               if (!fast) {
                 GroupSync<G>::sync();
