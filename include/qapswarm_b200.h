@@ -89,6 +89,7 @@ typedef struct qsb_state {
   void* swarm_min;           /* (m,) scratch */
   int64_t* swarm_min_idx;    /* (m,) scratch */
   uint32_t* done;            /* (1,) scratch, zero-initialised */
+  uint32_t* work;            /* (1,) scratch for dynamic particle scheduling, or NULL */
 } qsb_state;
 
 /* QAP instance on the device (qaplib.QapInstance, qaplib.py:28-69). */
@@ -114,6 +115,10 @@ typedef struct qsb_coeffs {
 /* |c1 * v| <= v_max holds for every stored velocity entry, so the clamp of
  * the rows untouched by x / pl / pg is a no-op and may be skipped. */
 #define QSB_HINT_V_BOUNDED 1
+/* st->cost[p] holds the goal of st->perm[p] on entry (true between engine
+ * steps), so the new goal may be computed incrementally from the facilities
+ * that moved (integral instances). */
+#define QSB_HINT_COST_CURRENT 2
 
 /* One migration event (migration.migrate, migration.py:55-86). */
 typedef struct qsb_migration {

@@ -20,6 +20,7 @@ QSB_OK, QSB_EINVAL, QSB_EUNSUPPORTED, QSB_ECUDA, QSB_EPERM = 0, 1, 2, 3, 4
 F32, F64, I64, U16 = 1, 2, 3, 4
 PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 4, 8, 16
 HINT_V_BOUNDED = 1
+HINT_COST_CURRENT = 2
 TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V
 
@@ -40,6 +41,7 @@ class QsbState(ctypes.Structure):
         ("pg_perm", _vp), ("pg_cost", _vp),
         ("best_perm", _vp), ("best_cost", _vp), ("best_iter", _vp), ("best_idx", _vp),
         ("iteration", _vp), ("swarm_min", _vp), ("swarm_min_idx", _vp), ("done", _vp),
+        ("work", _vp),
     ]
 
 

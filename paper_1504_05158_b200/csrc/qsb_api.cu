@@ -166,6 +166,16 @@ const char* qsb_strerror(int code) {
 
 int qsb_last_cuda_error(void) { return g_last_cuda; }
 
+#ifdef QSB_COUNTERS
+// diagnosis builds only: read and reset the step-kernel event counters
+int qsb_debug_counters(unsigned long long* out8) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, qsb_counters, 8 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_status(e);
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return cuda_status(cudaMemcpyToSymbol(qsb_counters, z, sizeof(z)));
+}
+#endif
+
 int32_t qsb_vstride(int32_t n, int32_t v_dtype) { return vstride_of(n, v_dtype); }
 
 int qsb_supported(int32_t n, int32_t v_dtype, int32_t mat_dtype) {
@@ -199,6 +209,7 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.D = inst ? inst->distance : nullptr;
   a.acc32 = inst ? inst->acc32 : 0;
   a.v_bounded = (co->hints & QSB_HINT_V_BOUNDED) ? 1 : 0;
+  a.cost_incremental = (co->hints & QSB_HINT_COST_CURRENT) ? 1 : 0;
 }
 
 int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co,
@@ -217,6 +228,11 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
   a.inj_stride = inj_stride;
   a.agg_base = agg_base;
   a.coef = coef;
+  a.work = st->work;
+  if (a.work) {
+    cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
   const int mat = inst ? inst->mat_dtype : QSB_U16;
   return dispatch<false>(st->v_dtype, mat, a, (cudaStream_t)stream);
 }

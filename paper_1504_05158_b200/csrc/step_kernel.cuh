@@ -69,6 +69,8 @@ struct StepArgs {
   int fd_smem;               // 1: stage F, D in smem; 0: read them from global/L2
   int v_bounded;             // host guarantee: |c1 * v| <= v_max for every stored v
   int acc32;                 // host guarantee: n * max(F) * max(D) < 2^32
+  int cost_incremental;      // host guarantee: cost[p] == goal(perm[p]) on entry
+  unsigned int* work;        // optional zeroed counter: dynamic particle scheduling
 };
 
 struct Best {
@@ -169,6 +171,16 @@ struct GroupSync {
     if constexpr (G == 1) __syncwarp(); else __syncthreads();
   }
 };
+
+// Optional event counters for diagnosis builds (-DQSB_COUNTERS): particles,
+// normal rounds, bulk steps, bulk z cells, tie rounds, warp tie paths,
+// slow tie paths, rescans.
+#ifdef QSB_COUNTERS
+__device__ unsigned long long qsb_counters[8];
+#define QSB_COUNT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&qsb_counters[i], (unsigned long long)(v)); } while (0)
+#else
+#define QSB_COUNT(i, v) do { } while (0)
+#endif
 
 #ifndef QSB_MINB
 #define QSB_MINB 4
@@ -465,7 +477,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
 // tid 0 (as raw bits for doubles).
 template <typename MT, int G, int CPL, typename Scratch>
 __device__ __noinline__ int64_t cost_general(const MT* cF, const MT* cD, int n, Scratch& sc,
-                                             int tid, int lane) {
+                                             int tid, int lane, int acc32) {
   constexpr int NT = 32 * G;
   if constexpr (std::is_floating_point<MT>::value) {
     double acc = 0.0;
@@ -482,11 +494,19 @@ __device__ __noinline__ int64_t cost_general(const MT* cF, const MT* cD, int n, 
     uint64_t part = 0;
     for (int j = tid; j < n; j += NT) {
       const int pj = sc.sperm[j];
-      for (int i = 0; i < n; ++i) {
-        if constexpr (sizeof(MT) <= 2)
-          part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj]);
-        else
-          part += (uint64_t)cF[i * n + j] * (uint64_t)cD[sc.sperm[i] * n + pj];
+      if (sizeof(MT) <= 2 && acc32) {
+        // n * max(F) * max(D) < 2^32: the column sum fits 32 bits
+        uint32_t p32 = 0;
+        for (int i = 0; i < n; ++i)
+          p32 += (uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj];
+        part += p32;
+      } else {
+        for (int i = 0; i < n; ++i) {
+          if constexpr (sizeof(MT) <= 2)
+            part += (uint64_t)((uint32_t)cF[i * n + j] * (uint32_t)cD[sc.sperm[i] * n + pj]);
+          else
+            part += (uint64_t)cF[i * n + j] * (uint64_t)cD[sc.sperm[i] * n + pj];
+        }
       }
     }
     int64_t tot = warp_sum_i64((int64_t)part);
@@ -499,6 +519,48 @@ __device__ __noinline__ int64_t cost_general(const MT* cF, const MT* cD, int n, 
     }
     return tot;
   }
+}
+
+// Column statistics for the uncommon cases (raw mode: no scaling; or some
+// column summed to 0): optional per-column scaling, then max / tie count /
+// first row over the non-z rows.  Out of line to keep the hot kernel small.
+template <typename VT, int CPL>
+struct ColIn {
+  int col[CPL], zr[CPL];
+  bool cfree[CPL], scale[CPL];
+  VT total[CPL], inv[CPL];
+};
+template <typename VT, int CPL>
+struct ColOut {
+  VT m[CPL];
+  int c[CPL], r[CPL];
+};
+
+template <typename VT, int CPL>
+__device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const ColIn<VT, CPL> in) {
+  const VT NINF = (VT)(-INFINITY);
+  ColOut<VT, CPL> o;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) { o.m[k] = NINF; o.c[k] = 0; o.r[k] = -1; }
+  for (int r = 0; r < n; ++r) {
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      if (!in.cfree[k]) continue;
+      VT* cell = tile + r * n + in.col[k];
+      VT v = *cell;
+      if (in.scale[k]) {
+        if constexpr (sizeof(VT) == 8) v = __ddiv_rn(v, in.total[k]);
+        else v = v * in.inv[k];
+        *cell = v;
+      }
+      const VT w = r == in.zr[k] ? NINF : v;
+      const bool gt = w > o.m[k];
+      o.c[k] = gt ? 1 : o.c[k] + (w == o.m[k] ? 1 : 0);
+      o.r[k] = gt ? r : o.r[k];
+      o.m[k] = gt ? w : o.m[k];
+    }
+  }
+  return o;
 }
 
 // ------------------------------------------------------------------------
@@ -556,7 +618,28 @@ step_kernel(const StepArgs a) {
   uint32_t phase = 0;
   int par = 0;
 
-  for (int64_t p = (int64_t)blockIdx.x * W + gidx; p < a.P; p += ngroups) {
+  // Particle scheduling: a shared work counter when given (per-particle cost
+  // varies with ties and rescans; dynamic assignment removes the tail),
+  // else a static grid stride.  The next index is claimed when a particle
+  // starts, so the atomic's latency is hidden behind the particle's work.
+  auto claim = [&]() -> unsigned {
+    unsigned q = 0;
+    if (tid == 0) q = atomicAdd(a.work, 1u);
+    return q;
+  };
+  auto bcast = [&](unsigned q) -> int64_t {
+    if constexpr (G == 1) {
+      return (int64_t)__shfl_sync(FULL, q, 0);
+    } else {
+      __syncthreads();
+      if (tid == 0) sc.ssel[1] = (int)q;
+      __syncthreads();
+      return (int64_t)(unsigned)sc.ssel[1];
+    }
+  };
+  int64_t p = a.work ? bcast(claim()) : (int64_t)blockIdx.x * W + gidx;
+  while (p < a.P) {
+    const unsigned q_next = a.work ? claim() : 0u;
     VT* gV = reinterpret_cast<VT*>(a.V) + p * a.vstride;
     if constexpr (GT) {
       tile = gV;
@@ -566,6 +649,7 @@ step_kernel(const StepArgs a) {
       bulk_load(tile, gV, tile_bytes, &sc.bar);
     }
 
+    QSB_COUNT(0, 1);
     DrawRow dr;
     dr.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
     dr.seed = a.seed;
@@ -660,32 +744,39 @@ step_kernel(const StepArgs a) {
             vg[k] = tile[pgr[k] * n + col[k]];
           }
         }
-        if (a.v_bounded) {
-          // |c1 v| <= v_max is guaranteed for every stored v: no clamp
-#pragma unroll 2
-          for (int r = 0; r < n; ++r) {
+        // two partial sums per column (even / odd rows) break the FADD
+        // dependency chain; the fp32 tolerance admits any summation order
+        float tot2[CPL];
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              if (!cfree[k]) continue;
-              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float lin = c1f * *cell;
-              *cell = lin;
-              tot[k] += fabsf(lin);
-            }
-          }
-        } else {
-#pragma unroll 2
-          for (int r = 0; r < n; ++r) {
+        for (int k = 0; k < CPL; ++k) tot2[k] = 0.f;
+        // |c1 v| <= v_max guaranteed for every stored v: the clamp is a no-op
+        const float vmc = a.v_bounded ? __int_as_float(0x7f800000) : vm;
+        int r = 0;
+        for (; r + 1 < n; r += 2) {
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              if (!cfree[k]) continue;
-              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float lin = fminf(fmaxf(c1f * *cell, -vm), vm);
-              *cell = lin;
-              tot[k] += fabsf(lin);
-            }
+          for (int k = 0; k < CPL; ++k) {
+            if (!cfree[k]) continue;
+            float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+            const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
+            const float l1 = fminf(fmaxf(c1f * cell[n], -vmc), vmc);
+            cell[0] = l0;
+            cell[n] = l1;
+            tot[k] += fabsf(l0);
+            tot2[k] += fabsf(l1);
           }
         }
+        if (r < n) {
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            if (!cfree[k]) continue;
+            float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+            const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
+            cell[0] = l0;
+            tot[k] += fabsf(l0);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) tot[k] += tot2[k];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           if (!cfree[k]) continue;
@@ -727,30 +818,76 @@ step_kernel(const StepArgs a) {
       else return v * inv[k];
     };
     if (do_agg) {
+      // Max / tie count / first row over the non-z rows (the z row is masked
+      // to -inf; stored values are finite), accumulated separately over even
+      // and odd rows (two independent dependency chains) and merged.  A
+      // half holding only the z row keeps max = -inf and is ignored.
       const VT NINF = (VT)(-INFINITY);
-#pragma unroll 2
-      for (int r = 0; r < n; ++r) {
+      VT mB[CPL];
+      int cB[CPL], rB[CPL];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) { mB[k] = NINF; cB[k] = 0; rB[k] = -1; }
+      auto upd = [&](VT v, int r, int k, VT& m, int& c, int& rr) {
+        const VT w = r == zr[k] ? NINF : v;
+        const bool gt = w > m;
+        c = gt ? 1 : c + (w == m ? 1 : 0);
+        rr = gt ? r : rr;
+        m = gt ? w : m;
+      };
+      auto stats_rows = [&](auto do_scale) {
+        int r = 0;
+        for (; r + 1 < n; r += 2) {
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            if (!cfree[k]) continue;
+            VT* cell = tile + r * n + col[k];
+            VT v0 = cell[0], v1 = cell[n];
+            if constexpr (decltype(do_scale)::value) {
+              v0 = rescale(v0, k); v1 = rescale(v1, k);
+              cell[0] = v0; cell[n] = v1;
+            }
+            upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
+            upd(v1, r + 1, k, mB[k], cB[k], rB[k]);
+          }
+        }
+        if (r < n) {
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            if (!cfree[k]) continue;
+            VT* cell = tile + r * n + col[k];
+            VT v0 = cell[0];
+            if constexpr (decltype(do_scale)::value) { v0 = rescale(v0, k); cell[0] = v0; }
+            upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
+          }
+        }
+      };
+      bool all_scale = true;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) all_scale &= scale[k] || !cfree[k];
+      if (__all_sync(FULL, all_scale)) {
+        stats_rows(std::true_type{});   // the normalised (norm mode) hot path
+      } else {
+        ColIn<VT, CPL> in;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          if (!cfree[k]) continue;
-          VT* cell = tile + r * n + col[k];
-          VT v = *cell;
-          if (scale[k]) { v = rescale(v, k); *cell = v; }
-          const VT w = r == zr[k] ? NINF : v;
-          const bool gt = w > nmax[k];
-          // (a -inf == -inf tie before the first non-z row is reset by gt)
-          ncnt[k] = gt ? 1 : ncnt[k] + (w == nmax[k] ? 1 : 0);
-          nrow[k] = gt ? r : nrow[k];
-          nmax[k] = gt ? w : nmax[k];
+          in.col[k] = col[k]; in.zr[k] = zr[k]; in.cfree[k] = cfree[k]; in.scale[k] = scale[k];
+          in.total[k] = total[k]; in.inv[k] = inv[k];
         }
+        const ColOut<VT, CPL> o = stats_generic<VT, CPL>(tile, n, in);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) { nmax[k] = o.m[k]; ncnt[k] = o.c[k]; nrow[k] = o.r[k]; }
       }
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
+        // merge the odd-row half (ties: counts add, first row = smaller row)
+        if (nmax[k] == NINF || mB[k] > nmax[k]) { nmax[k] = mB[k]; ncnt[k] = cB[k]; nrow[k] = rB[k]; }
+        else if (mB[k] == nmax[k] && mB[k] != NINF) { ncnt[k] += cB[k]; nrow[k] = min(nrow[k], rB[k]); }
         nk64[k] = ncnt[k] ? nonz_key(nmax[k]) : 0;
         zkey[k] = z_key(tile[zr[k] * n + col[k]]);
       }
     } else {
+#pragma unroll 1
       for (int r = 0; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
@@ -859,6 +996,8 @@ step_kernel(const StepArgs a) {
                 const uint64_t rmask = ((uint64_t)rh << 32) | rl;
                 rf.w[0] &= ~rmask;
                 rnd += nq - 1;
+                QSB_COUNT(2, 1);
+                QSB_COUNT(3, nq);
                 // non-z statistics whose maximum row may have left
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) {
@@ -871,6 +1010,7 @@ step_kernel(const StepArgs a) {
           }
 
           if (!bulk) {
+            QSB_COUNT(1, 1);
             // ---- one round: lane-local best of the cached candidates, then the group's
             Best loc;
             loc.key = ck[0]; loc.cnt = cc[0]; loc.col = col[0]; loc.row = cr[0];
@@ -910,6 +1050,7 @@ step_kernel(const StepArgs a) {
               const double u = dr.at(cursor++);
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
+              QSB_COUNT(4, 1);
               bool fast = false;
               sel_r = sel_c = -1;
               if constexpr (G == 1 && CPL <= 2) {
@@ -940,6 +1081,7 @@ step_kernel(const StepArgs a) {
 #pragma unroll
                   for (int k = 0; k < CPL; ++k)
                     if (cc[k] && ck[k] == b.key) sc.stie[col[k]] = zel[k] ? 2 : 1;
+                  QSB_COUNT(5, 1);
                   const int rc = tie_select_warp<VT>(tile, n, sc, rf.w[0], b.key, pick, lane);
                   sel_r = rc >> 8;
                   sel_c = rc & 0xff;
@@ -951,6 +1093,7 @@ step_kernel(const StepArgs a) {
 #pragma unroll
                 for (int k = 0; k < CPL; ++k)
                   if (cc[k] && ck[k] == b.key) sc.stie[col[k]] = zel[k] ? 2 : 1;
+                QSB_COUNT(6, 1);
                 tie_select_slow<VT, G, NW>(tile, n, sc, rf, b.key, pick, tid);
                 sel_r = sc.ssel[0]; sel_c = sc.ssel[1];
                 GroupSync<G>::sync();
@@ -989,6 +1132,7 @@ step_kernel(const StepArgs a) {
               while (mask) {
                 const int src = __ffs(mask) - 1;
                 mask &= mask - 1;
+                QSB_COUNT(7, 1);
                 const int c = src + k * 32;
                 const int zc = __shfl_sync(FULL, zr[k], src);
                 if constexpr (sizeof(VT) == 4) {
@@ -1071,42 +1215,68 @@ step_kernel(const StepArgs a) {
       }
       Sync::sync();
       int16_t* gnew = a.perm_new + p * n;
+      #pragma unroll 1
       for (int c = tid; c < n; c += NT) gnew[c] = (int16_t)sc.sperm[c];
     }
 
     // ================= phase 3: goal  sum_ij F[i,j] * D[perm_i, perm_j]
-    if (do_cost) {
-      bool fast = false;
-      if constexpr (sizeof(MT) <= 2 && !kFloatMat) fast = a.acc32 != 0;
-      if (fast) {
-        // n * max(F) * max(D) < 2^32: per-column sums fit 32 bits; the row
-        // index perm[i] is loaded once for all owned columns
-        int pj[CPL];
-        uint32_t p32[CPL];
+    bool cost_done = false;
+    if constexpr (G == 1 && !kFloatMat) {
+      // Incremental goal (integral instances, one-warp groups): most columns
+      // keep their row (the bulk step re-selects the z cells), so with C the
+      // set of facilities that moved,
+      //   cost' - cost = sum_{i in C, all j} F[i][j] (D'[i][j] - D[i][j])
+      //                + sum_{i not in C, j in C} F[i][j] (D'[i][j] - D[i][j])
+      // with D[i][j] = D[p_i][p_j].  Exact in int64 (mod 2^64, as the full
+      // sum).  Needs cost[p] == goal(perm[p]) on entry (host guarantee).
+      if (do_cost && a.cost_incremental) {
+        Sync::sync();
+        const int c0 = lane, c1 = lane + 32;
+        const bool m0 = c0 < n && sc.sperm[c0] != sc.szr[c0];
+        const bool m1 = c1 < n && sc.sperm[c1] != sc.szr[c1];
+        const unsigned ch[2] = {__ballot_sync(FULL, m0), __ballot_sync(FULL, m1)};
+        const int k = __popc(ch[0]) + __popc(ch[1]);
+        if (3 * k <= n) {
+          uint64_t acc = 0;
+          int pjn[CPL], pjo[CPL];
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) { pj[k] = col[k] < n ? sc.sperm[col[k]] : 0; p32[k] = 0; }
-        for (int i = 0; i < n; ++i) {
-          const MT* Frow = cF + i * n;
-          const MT* Drow = cD + sc.sperm[i] * n;
+          for (int kk = 0; kk < CPL; ++kk) {
+            pjn[kk] = col[kk] < n ? sc.sperm[col[kk]] : 0;
+            pjo[kk] = col[kk] < n ? sc.szr[col[kk]] : 0;
+          }
+          const int ro0 = c0 < n ? sc.szr[c0] : 0, ro1 = c1 < n ? sc.szr[c1] : 0;
 #pragma unroll
-          for (int k = 0; k < CPL; ++k)
-            if (col[k] < n) p32[k] += (uint32_t)Frow[col[k]] * (uint32_t)Drow[pj[k]];
+          for (int h = 0; h < 2; ++h) {
+            unsigned b = ch[h];
+            while (b) {
+              const int i = h * 32 + __ffs(b) - 1;
+              b &= b - 1;
+              const int pin = sc.sperm[i], pio = sc.szr[i];
+              // row i of the changed facilities, every column (owned by lanes)
+#pragma unroll
+              for (int kk = 0; kk < CPL; ++kk)
+                if (col[kk] < n)
+                  acc += (uint64_t)cF[i * n + col[kk]] *
+                         (uint64_t)((int64_t)cD[pin * n + pjn[kk]] - (int64_t)cD[pio * n + pjo[kk]]);
+              // column i, rows that did not move (lanes own rows lane, lane+32)
+              if (c0 < n && !m0)
+                acc += (uint64_t)cF[c0 * n + i] * (uint64_t)((int64_t)cD[ro0 * n + pin] - (int64_t)cD[ro0 * n + pio]);
+              if (c1 < n && !m1)
+                acc += (uint64_t)cF[c1 * n + i] * (uint64_t)((int64_t)cD[ro1 * n + pin] - (int64_t)cD[ro1 * n + pio]);
+            }
+          }
+          const int64_t delta = warp_sum_i64((int64_t)acc);
+          if (tid == 0) {
+            int64_t* cp = reinterpret_cast<int64_t*>(a.cost);
+            cp[p] = (int64_t)((uint64_t)cp[p] + (uint64_t)delta);
+          }
+          cost_done = true;
         }
-        uint64_t part = 0;
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) part += p32[k];
-        int64_t tot = warp_sum_i64((int64_t)part);
-        if constexpr (G > 1) {
-          if (lane == 0) sc.lslots[tid >> 5] = tot;
-          __syncthreads();
-          tot = 0;
-          for (int w = 0; w < G; ++w) tot += sc.lslots[w];
-        }
-        if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;
-      } else {
-        const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane);
-        if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
       }
+    }
+    if (do_cost && !cost_done) {
+      const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane, a.acc32);
+      if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
     }
 
     // ================= phase 4a: personal best (engine.py:211-215)
@@ -1131,10 +1301,12 @@ step_kernel(const StepArgs a) {
       Sync::sync();
       if (sc.ssel[2]) {
         int16_t* gpl = a.pl_perm + p * n;
+        #pragma unroll 1
         for (int c = tid; c < n; c += NT) gpl[c] = (int16_t)sc.sperm[c];
       }
     }
     Sync::sync();
+    p = a.work ? bcast(q_next) : p + ngroups;
   }
   if (!GT && tid == 0) bulk_wait_all();
 }

@@ -138,6 +138,7 @@ class PopulationState:
             self.d_swarm_min = torch.zeros(self.local_swarms, dtype=cdt, **z)
             self.d_swarm_min_idx = torch.zeros(self.local_swarms, dtype=torch.int64, **z)
             self.d_done = torch.zeros(1, dtype=torch.int32, **z)
+            self.d_work = torch.zeros(1, dtype=torch.int32, **z)
         except torch.OutOfMemoryError:
             raise MemoryError(
                 f"cannot allocate population buffers: {p} particles of size {n}x{n} need about "
@@ -151,6 +152,7 @@ class PopulationState:
         self._cs = None
         self.launches = 0         # kernels launched by step() (bench accounting)
         self.v_bound = float("inf")   # proven bound on max |V| (enables QSB_HINT_V_BOUNDED)
+        self.cost_current = False     # cost[p] == goal(perm[p]) (enables QSB_HINT_COST_CURRENT)
 
     # ---------------------------------------------------------- C structs
     def c_state(self) -> _lib.QsbState:
@@ -167,7 +169,7 @@ class PopulationState:
         s.swarm_offset = self.swarm_offset
         for name in ("V", "perm", "perm_new", "pl_perm", "cost", "pl_cost", "improved",
                      "pg_perm", "pg_cost", "best_perm", "best_cost", "best_iter", "best_idx",
-                     "swarm_min", "swarm_min_idx", "done"):
+                     "swarm_min", "swarm_min_idx", "done", "work"):
             setattr(s, name, _ptr(getattr(self, "d_" + name)))
         s.iteration = _ptr(self.d_iteration)
         self._cs = s
@@ -340,6 +342,7 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
     state.t = 0
     state._host_best = None
     state.v_bound = float(config.init_velocity_amplitude)
+    state.cost_current = True
     costs = state.d_cost.cpu().numpy()
     if state.local_particles != state.num_particles and torch.distributed.is_initialized():
         lo = torch.tensor([costs.min(), -costs.max()], dtype=torch.float64, device=state.device)
@@ -456,7 +459,10 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     stream = state.stream()
     cs = state.c_state()
     # |c1 v| <= v_max for every stored v => the bulk-row clamp is a no-op
-    rt.coeffs.hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
+    hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
+    if state.cost_current and state.integral:
+        hints |= _lib.HINT_COST_CURRENT
+    rt.coeffs.hints = hints
     passes = config.two_opt_passes
     if passes and not state.integral:
         raise ValueError("two_opt_passes requires an integral instance")
