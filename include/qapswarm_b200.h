@@ -187,6 +187,17 @@ int qsb_twoopt(const qsb_state* st, const qsb_instance* inst, int32_t passes, in
 /* Goal of P permutations (int16, device) -> out (int64 or f64, device). */
 int qsb_cost(const int16_t* perms, int64_t P, const qsb_instance* inst, void* out, void* stream);
 
+/* Population statistics on the device (stats.collect, stats.py:72-100):
+ * hist[bins] = the frozen-range PMF counts, binned exactly as numpy
+ * (stats.py:45-47); out[0] = the minimum cost; out[1 + r] = the
+ * ranks_k[r]-th smallest cost (0-based; nearest-rank percentile, stats.py:28),
+ * r < nranks <= 4.  Values are the cost's raw 64-bit pattern (int64 or f64).
+ * `work` is device scratch of qsb_stats_work_bytes() bytes. */
+size_t qsb_stats_work_bytes(void);
+int qsb_population_stats(const void* cost, int32_t cost_dtype, int64_t P, double lo, double width,
+                         int32_t bins, const int64_t* ranks_k, int32_t nranks, void* work,
+                         uint32_t* hist, int64_t* out, void* stream);
+
 /* streams.step_draws rows p0 .. p0+P-1 into device memory. */
 int qsb_step_draws(uint64_t seed, uint64_t t, int64_t p0, int64_t P, int32_t n, double* out,
                    void* stream);

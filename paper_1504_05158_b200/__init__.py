@@ -20,6 +20,7 @@ from .engine import (
     projected_buffer_bytes,
     device_buffer_bytes,
     gap,
+    collect_device,
 )
 from . import batch
 
@@ -31,5 +32,5 @@ __all__ = [
     "SwarmBestTable", "MigrationEvent", "migrate",
     "IterationStats", "percentile", "pmf", "collect", "export_csv", "write_solution",
     "PopulationState", "RunResult", "init_population", "step", "run",
-    "projected_buffer_bytes", "device_buffer_bytes", "gap", "batch",
+    "projected_buffer_bytes", "device_buffer_bytes", "gap", "batch", "collect_device",
 ]

@@ -82,6 +82,9 @@ SIGNATURES = {
                                   _i32, _vp]),
     "qsb_twoopt_many": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32]),
     "qsb_step_draws": (ctypes.c_int, [_u64, _u64, _i64, _i64, _i32, _vp, _vp]),
+    "qsb_stats_work_bytes": (ctypes.c_size_t, []),
+    "qsb_population_stats": (ctypes.c_int, [_vp, _i32, _i64, _dbl, _dbl, _i32, _vp, _i32, _vp,
+                                            _vp, _vp, _vp]),
     "qsb_init_population_device": (ctypes.c_int, [ctypes.POINTER(QsbState), _u64, _dbl, _vp]),
     "qsb_perm_to_matrix": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "qsb_velocity_many": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i64, _dbl, _vp, _vp,

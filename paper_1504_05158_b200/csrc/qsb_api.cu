@@ -9,6 +9,7 @@
 #include "aux_kernels.cuh"
 #include "step_kernel.cuh"
 #include "twoopt.cuh"
+#include "stats.cuh"
 
 using namespace qsb;
 
@@ -321,6 +322,50 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(migrate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     migrate_kernel<double><<<1, 1024, smem, s>>>(a);
+  }
+  return launch_status();
+}
+
+size_t qsb_stats_work_bytes(void) { return sizeof(StatsWork); }
+
+int qsb_population_stats(const void* cost, int32_t cost_dtype, int64_t P, double lo, double width,
+                         int32_t bins, const int64_t* ranks_k, int32_t nranks, void* work,
+                         uint32_t* hist, int64_t* out, void* stream) {
+  if (!cost || !work || !hist || !out || P <= 0 || bins < 1 || nranks < 0 || nranks > STATS_RANKS ||
+      !(width > 0.0))
+    return QSB_EINVAL;
+  if (nranks && !ranks_k) return QSB_EINVAL;
+  unsigned long long k[STATS_RANKS] = {0, 0, 0, 0};
+  for (int r = 0; r < nranks; ++r) {
+    if (ranks_k[r] < 0 || ranks_k[r] >= P) return QSB_EINVAL;
+    k[r] = (unsigned long long)ranks_k[r];
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  StatsWork* w = (StatsWork*)work;
+  cudaError_t e = cudaMemsetAsync(w, 0, sizeof(StatsWork), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)bins, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  stats_init_kernel<<<1, 1, 0, s>>>(w, k[0], k[1], k[2], k[3]);
+  const int threads = 256;
+  const int grid = (int)((P + threads - 1) / threads < 2 * num_sms() ? (P + threads - 1) / threads : 2 * num_sms());
+  const size_t hsmem = sizeof(unsigned int) * (size_t)bins;
+  if (hsmem > smem_optin()) return QSB_EUNSUPPORTED;
+  if (cost_dtype == QSB_I64) {
+    auto hk = stats_hist_kernel<int64_t>;
+    if (hsmem > 48 * 1024) cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    hk<<<grid, threads, hsmem, s>>>((const int64_t*)cost, P, lo, width, bins, hist, w);
+    for (int shift = 56; nranks && shift >= 0; shift -= 8)
+      stats_select_kernel<int64_t><<<grid, threads, 0, s>>>((const int64_t*)cost, P, shift, nranks, w);
+    stats_finish_kernel<int64_t><<<1, 1, 0, s>>>(w, nranks, (long long*)out);
+  } else if (cost_dtype == QSB_F64) {
+    auto hk = stats_hist_kernel<double>;
+    if (hsmem > 48 * 1024) cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    hk<<<grid, threads, hsmem, s>>>((const double*)cost, P, lo, width, bins, hist, w);
+    for (int shift = 56; nranks && shift >= 0; shift -= 8)
+      stats_select_kernel<double><<<grid, threads, 0, s>>>((const double*)cost, P, shift, nranks, w);
+    stats_finish_kernel<double><<<1, 1, 0, s>>>(w, nranks, (long long*)out);
+  } else {
+    return QSB_EINVAL;
   }
   return launch_status();
 }

@@ -24,6 +24,7 @@ permutations are materialised on demand by the host-view properties of
 
 from __future__ import annotations
 
+import math
 import time
 from dataclasses import dataclass, field
 
@@ -34,7 +35,7 @@ from . import _lib
 from .config import SX_CODES, PsoCoefficients, SolverConfig
 from .instance import device_format, is_integral
 from .migration import MigrationEvent, SwarmBestTable
-from .stats import IterationStats, collect
+from .stats import PERCENTILE_RANKS, IterationStats, _ranks_sorted, collect
 
 PHASE_INIT, PHASE_STEP, PHASE_HOST = 1, 2, 3
 _ITER_LIMIT = 1 << 32
@@ -150,6 +151,7 @@ class PopulationState:
         self._host_best = None    # cached (cost, iteration, perm) of the device record
         self._inst = None
         self._cs = None
+        self._stats_scratch = None
         self.launches = 0         # kernels launched by step() (bench accounting)
         self.v_bound = float("inf")   # proven bound on max |V| (enables QSB_HINT_V_BOUNDED)
         self.cost_current = False     # cost[p] == goal(perm[p]) (enables QSB_HINT_COST_CURRENT)
@@ -438,6 +440,56 @@ def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchan
     state._mig.pending += 1
 
 
+# ------------------------------------------------------------ statistics
+def collect_device(state: PopulationState, time_ms: float, bins: int = 60,
+                   all_swarms: bool = False) -> IterationStats:
+    """stats.collect (stats.py:72-100) with the O(P) parts on the device: the
+    PMF histogram, the minimum and the four nearest-rank percentiles come
+    from qsb_population_stats; only the swarm-best table and the best
+    swarm's costs cross to the host.  Field values and types are identical to
+    :func:`stats.collect` (same float64 binning, same k-th smallest)."""
+    import ctypes
+    P = state.local_particles
+    lo, hi = state.pmf_range
+    if bins < 1:
+        raise ValueError(f"bins must be >= 1, got {bins}")
+    if not lo < hi:
+        raise ValueError(f"invalid range: [{lo}, {hi}]")
+    width = (hi - lo) / bins
+    ks = [math.ceil(r / 100.0 * P) - 1 for r in PERCENTILE_RANKS]
+    sc = state._stats_scratch
+    if sc is None or sc[1].numel() < bins:
+        work = torch.empty(int(_lib.lib().qsb_stats_work_bytes()), dtype=torch.uint8, device=state.device)
+        sc = (work, torch.empty(max(bins, 64), dtype=torch.int32, device=state.device),
+              torch.empty(8, dtype=torch.int64, device=state.device))
+        state._stats_scratch = sc
+    work, hist, out = sc
+    karr = (ctypes.c_int64 * 4)(*ks)
+    _lib.call("qsb_population_stats", state.d_cost.data_ptr(), state.cost_code, P, float(lo),
+              float(width), bins, karr, 4, work.data_ptr(), hist.data_ptr(), out.data_ptr(),
+              state.stream())
+    vals = out.cpu().numpy()[:5]
+    if state.cost_code == _lib.F64:
+        vals = vals.view(np.float64)
+    counts = hist[:bins].cpu().numpy().astype(np.int64)
+    freq = counts / P
+    edges = lo + width * np.arange(bins + 1)
+    table = state.d_pg_cost.cpu().numpy()
+    best_swarm = int(np.argmin(table))
+    S = state.swarm_size
+    mine = state.d_cost[best_swarm * S:(best_swarm + 1) * S].cpu().numpy()
+    all_ranks = None
+    if all_swarms:
+        srt = np.sort(state.d_cost.cpu().numpy().reshape(state.swarms, S), axis=1)
+        all_ranks = np.array([_ranks_sorted(row) for row in srt], dtype=np.float64)
+    p5, p25, p50, p75 = (vals[1 + i].item() for i in range(4))
+    return IterationStats(
+        t=state.t, p5=p5, p25=p25, p50=p50, p75=p75, best=vals[0].item(),
+        global_best=state.best_cost, per_swarm_best=table.copy(), pmf_edges=edges, pmf_freq=freq,
+        time_ms=time_ms, best_swarm=best_swarm,
+        best_swarm_percentiles=tuple(_ranks_sorted(np.sort(mine))), all_swarm_percentiles=all_ranks)
+
+
 # ------------------------------------------------------------------ step
 def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
          timer=None) -> PopulationState:
@@ -526,8 +578,9 @@ def run(config: SolverConfig, instance, collect_stats: bool = True, device=None)
     state = init_population(config, instance, device)
     series: list[IterationStats] = []
     if collect_stats:
-        series.append(collect(state, 1000.0 * (time.perf_counter() - t_start),
-                              bins=config.pmf_bins, all_swarms=config.record_all_swarm_percentiles))
+        series.append(collect_device(state, 1000.0 * (time.perf_counter() - t_start),
+                                     bins=config.pmf_bins,
+                                     all_swarms=config.record_all_swarm_percentiles))
     for _ in range(config.max_iterations):
         if config.target_cost is not None and state.best_cost <= config.target_cost:
             break
@@ -536,8 +589,8 @@ def run(config: SolverConfig, instance, collect_stats: bool = True, device=None)
         if collect_stats and state.t % config.stats_stride == 0:
             torch.cuda.current_stream(state.device).synchronize()
             elapsed_ms = 1000.0 * (time.perf_counter() - it_start)
-            series.append(collect(state, elapsed_ms, bins=config.pmf_bins,
-                                  all_swarms=config.record_all_swarm_percentiles))
+            series.append(collect_device(state, elapsed_ms, bins=config.pmf_bins,
+                                         all_swarms=config.record_all_swarm_percentiles))
     torch.cuda.current_stream(state.device).synchronize()
     total = time.perf_counter() - t_start
     _drain_log(state)

@@ -299,3 +299,29 @@ def test_step_with_twoopt_matches_oracle(passes, precision, golden_instances):
         assert np.array_equal(st.pl_cost, ost.pl_cost)
         assert np.array_equal(st.bests.costs, ost.pg_costs)
         assert st.best_cost == ost.best_cost
+
+
+# ------------------------------------------------------- device statistics
+@pytest.mark.parametrize("precision,instance", [("fp32", "tai50"), ("fp64", "float6"),
+                                                ("fp64", "chr12a")])
+def test_collect_device_equals_host_collect(precision, instance, golden_instances):
+    inst = golden_instances[instance]
+    swarms, S = (40, 25) if inst.n > 20 else (7, 9)
+    cfg = qsb.SolverConfig(swarms=swarms, swarm_size=S, seed=2, precision=precision,
+                           migration_factor=0.2,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    st = qsb.init_population(cfg, inst)
+    for t in range(4):
+        for bins in (1, 7, 60, 1000):
+            a = qsb.collect(st, 1.5, bins=bins, all_swarms=(t == 1))
+            b = qsb.collect_device(st, 1.5, bins=bins, all_swarms=(t == 1))
+            for f in ("t", "p5", "p25", "p50", "p75", "best", "global_best", "time_ms",
+                      "best_swarm", "best_swarm_percentiles"):
+                va, vb = getattr(a, f), getattr(b, f)
+                assert va == vb and type(va) is type(vb), (f, va, vb)
+            assert a.pmf_freq.tobytes() == b.pmf_freq.tobytes()
+            assert a.pmf_edges.tobytes() == b.pmf_edges.tobytes()
+            assert a.per_swarm_best.tobytes() == b.per_swarm_best.tobytes()
+            if t == 1:
+                assert a.all_swarm_percentiles.tobytes() == b.all_swarm_percentiles.tobytes()
+        qsb.step(st, inst, cfg)
