@@ -28,7 +28,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "particle-iterations/sec (QAP n=50, 80k particles)"
+METRIC = "particle-iterations/sec (QAP n=50, 80k particles)"   # the headline (config3)
 UNIT = "particle-iterations/s"
 N_DEFAULT, SWARMS, SWARM_SIZE = 50, 800, 100
 PERIOD, FACTOR, SEED = 10, 0.33, 1
@@ -49,7 +49,27 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--velocity-only", action="store_true",
                     help="time only the velocity/normalise phase of the fused kernel")
-    return ap.parse_args()
+    ap.add_argument("--preset", default="config3",
+                    choices=["config1", "config2", "config3", "config4", "config5"],
+                    help="BASELINE.json configs: 1 n=12 1x100; 2 n=30 100x100 2-opt; "
+                         "3 n=50 800x100 migration/10 (the headline, default); "
+                         "4 n=100 10k; 5 n=256 2k/GPU 2-opt + migration")
+    ap.add_argument("--two-opt", type=int, default=None)
+    args = ap.parse_args()
+    presets = {
+        "config1": dict(n=12, swarms=1, swarm_size=100, two_opt=0, factor=0.0),
+        "config2": dict(n=30, swarms=100, swarm_size=100, two_opt=1, factor=0.0),
+        "config3": dict(n=50, swarms=800, swarm_size=100, two_opt=0, factor=FACTOR),
+        "config4": dict(n=100, swarms=100, swarm_size=100, two_opt=0, factor=FACTOR),
+        "config5": dict(n=256, swarms=20, swarm_size=100, two_opt=1, factor=FACTOR),
+    }
+    pr = presets[args.preset]
+    if args.preset != "config3":
+        args.n, args.swarms, args.swarm_size = pr["n"], pr["swarms"], pr["swarm_size"]
+    args.factor = pr["factor"]
+    if args.two_opt is None:
+        args.two_opt = pr["two_opt"]
+    return args
 
 
 def config(args, swarms=None, precision=None):
@@ -58,14 +78,17 @@ def config(args, swarms=None, precision=None):
         swarms=swarms or args.swarms, swarm_size=args.swarm_size, seed=SEED,
         coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5, v_max=4.0, sv_mode="norm",
                                           sx_mode="second-target", depth=2),
-        migration_factor=FACTOR, migration_period=PERIOD,
-        precision=precision or args.precision, init="device")
+        migration_factor=getattr(args, "factor", FACTOR), migration_period=PERIOD,
+        precision=precision or args.precision, init="device",
+        two_opt_passes=getattr(args, "two_opt", 0))
 
 
 def workload(args, n_gpus):
+    mig = (f"migration f={args.factor} every {PERIOD} iterations" if args.factor
+           else "independent swarms")
     return {"workload": f"synthetic Taillard-style QAP n={args.n}, {args.swarms} swarms x "
-                        f"{args.swarm_size} particles, migration f={FACTOR} every {PERIOD} "
-                        f"iterations, sv=norm, sx=second-target(2), c=(0.8,0.5,0.5)",
+                        f"{args.swarm_size} particles, {mig}, sv=norm, sx=second-target(2), "
+                        f"c=(0.8,0.5,0.5), 2-opt passes={args.two_opt} ({args.preset})",
             "n": args.n, "particles": args.swarms * args.swarm_size, "swarms": args.swarms,
             "swarm_size": args.swarm_size, "precision": args.precision,
             "parallelism": f"swarm-shard x{n_gpus}",
@@ -381,7 +404,9 @@ def main():
     best = shard.merge_best(state.best_cost, state.best_iteration, 0, state.best_perm, world,
                             dev) if world > 1 else None
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        metric = METRIC if args.preset == "config3" else \
+            f"particle-iterations/sec (QAP n={args.n}, {P_total} particles, {args.preset})"
+        line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if cfg.precision == "fp32" else "f64", "data": "synthetic",

@@ -158,6 +158,7 @@ struct GroupScratch {
   unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
   uint64_t sbulk[NMAX];      // z keys assigned by bulk steps (pending tie-draw count)
   uint64_t tmask[NMAX];      // per tied column: mask of tied rows (one-warp tie path)
+  unsigned long long rmw[(NMAX + 63) / 64];   // rows retired by a bulk step (multi-warp groups)
   Best slots[2][G];
   int islots[2][G];
   int64_t lslots[G];
@@ -356,6 +357,27 @@ __device__ __noinline__ int bulk_distinct(const Scratch& sc, int nb, int lane) {
     distinct += __any_sync(FULL, v0 && e0 == v) ? 0 : 1;
   }
   return distinct;
+}
+
+// Same for multi-warp groups (n > 64): O(nb^2 / threads) comparisons.
+template <int G, typename Scratch>
+__device__ __noinline__ int bulk_distinct_group(Scratch& sc, int nb, int tid, int lane) {
+  constexpr int NT = 32 * G;
+  int firsts = 0;
+  for (int i = tid; i < nb; i += NT) {
+    const uint64_t ki = sc.sbulk[i];
+    bool first = true;
+    for (int j = 0; j < i; ++j) if (sc.sbulk[j] == ki) { first = false; break; }
+    firsts += first;
+  }
+  firsts = (int)__reduce_add_sync(FULL, (unsigned)firsts);
+  __syncthreads();
+  if (lane == 0) sc.islots[0][tid >> 5] = firsts;
+  __syncthreads();
+  int tot = 0;
+  for (int w = 0; w < G; ++w) tot += sc.islots[0][w];
+  __syncthreads();
+  return tot;
 }
 
 // Tie round for one-warp groups (n <= 64): the pick-th tied cell in
@@ -1007,6 +1029,52 @@ step_kernel(const StepArgs a) {
                 bulk = true;
               }
             }
+          } else {
+            // multi-warp groups: the same bulk step with smem reductions
+            if (!restricted) {
+              uint64_t ml = 0;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k)
+                if (cfree[k] && ncnt[k] && nk64[k] > ml) ml = nk64[k];
+              Best mb; mb.key = ml; mb.cnt = ml ? 1 : 0; mb.col = 0; mb.row = 0;
+              const uint64_t M = group_best<G>(mb, sc, par, lane, tid).key;
+              bool q[CPL];
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) q[k] = cfree[k] && zel[k] && zkey[k] > M;
+              if (tid == 0) sc.ssel[2] = 0;
+              if (tid < NW) sc.rmw[tid] = 0ULL;
+              __syncthreads();
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) {
+                if (!q[k]) continue;
+                const int pos = atomicAdd(&sc.ssel[2], 1);
+                sc.sbulk[nbulk + pos] = zkey[k];
+                atomicOr(&sc.rmw[zr[k] >> 6], 1ULL << (zr[k] & 63));
+              }
+              __syncthreads();
+              const int nq = sc.ssel[2];
+              if (nq >= 2) {
+                uint64_t rm[NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) { rm[w] = sc.rmw[w]; rf.w[w] &= ~rm[w]; }
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                  if (q[k]) {
+                    sc.sperm[col[k]] = zr[k];
+                    cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
+                  } else if (cfree[k] && ncnt[k]) {
+                    need[k] = (ncnt[k] == 1 && nrow[k] >= 0) ? ((rm[nrow[k] >> 6] >> (nrow[k] & 63)) & 1ULL)
+                                                             : true;
+                  }
+                }
+                nbulk += nq;
+                rnd += nq - 1;
+                QSB_COUNT(2, 1);
+                QSB_COUNT(3, nq);
+                bulk = true;
+              }
+              __syncthreads();
+            }
           }
 
           if (!bulk) {
@@ -1044,8 +1112,10 @@ step_kernel(const StepArgs a) {
                                                      tid, lane);
             } else {
               // ---- ties: one draw, the pick-th tied cell in row-major order
-              if constexpr (G == 1) {
-                if (nbulk) { cursor += nbulk - bulk_distinct(sc, nbulk, lane); nbulk = 0; }
+              if (nbulk) {
+                if constexpr (G == 1) cursor += nbulk - bulk_distinct(sc, nbulk, lane);
+                else cursor += nbulk - bulk_distinct_group<G>(sc, nbulk, tid, lane);
+                nbulk = 0;
               }
               const double u = dr.at(cursor++);
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);

@@ -75,6 +75,36 @@ __global__ void __launch_bounds__(NT) twoopt_kernel(const TwoOptArgs a) {
     for (int pass = 0; pass < a.passes; ++pass) {
       int64_t best = INT64_MAX;
       int bq = INT_MAX;
+      if (a.sym && n >= 96 && sizeof(MT) == 2 && (n % 2) == 0) {
+        // large symmetric n: one warp per pair, lanes over k (row streams
+        // F[r][.], F[s][.], Dp[r][.], Dp[s][.] are contiguous -> no bank
+        // conflicts; two uint16 per 32-bit load)
+        const unsigned* F32 = reinterpret_cast<const unsigned*>(F);
+        const unsigned* D32 = reinterpret_cast<const unsigned*>(Dp);
+        const int h = n / 2;
+        for (int64_t q = warp; q < npairs; q += NT / 32) {
+          int r, s;
+          unrank_pair(q, n, r, s);
+          int64_t acc = 0;
+          for (int j = lane; j < h; j += 32) {
+            const unsigned fr = F32[r * h + j], fs = F32[s * h + j];
+            const unsigned dr = D32[r * h + j], ds = D32[s * h + j];
+            const int k0 = 2 * j, k1 = 2 * j + 1;
+            const int64_t a0 = ((int64_t)(fr & 0xffff) - (int64_t)(fs & 0xffff)) *
+                               ((int64_t)(ds & 0xffff) - (int64_t)(dr & 0xffff));
+            const int64_t a1 = ((int64_t)(fr >> 16) - (int64_t)(fs >> 16)) *
+                               ((int64_t)(ds >> 16) - (int64_t)(dr >> 16));
+            acc += (k0 == r || k0 == s) ? 0 : a0;
+            acc += (k1 == r || k1 == s) ? 0 : a1;
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+          const int64_t dd = (int64_t)((uint64_t)((int64_t)F[r * n + r] - F[s * n + s]) *
+                                           (uint64_t)((int64_t)Dp[s * n + s] - Dp[r * n + r]) +
+                                       2 * (uint64_t)acc);
+          if (dd < best) { best = dd; bq = (int)q; }   // q ascends per warp: first wins
+        }
+      } else
       for (int64_t q = threadIdx.x; q < npairs; q += NT) {
         int r, s;
         unrank_pair(q, n, r, s);

@@ -325,3 +325,18 @@ def test_collect_device_equals_host_collect(precision, instance, golden_instance
             if t == 1:
                 assert a.all_swarm_percentiles.tobytes() == b.all_swarm_percentiles.tobytes()
         qsb.step(st, inst, cfg)
+
+
+@pytest.mark.parametrize("n", [96, 128, 256])
+def test_twoopt_large_symmetric_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    f = np.triu(rng.integers(0, 100, (n, n)), 1)
+    d = np.triu(rng.integers(0, 100, (n, n)), 1)
+    f, d = f + f.T, d + d.T
+    perms = np.array([rng.permutation(n) for _ in range(9)], dtype=np.int64)
+    costs = np.zeros(9, np.int64)
+    orc.cost_many(perms, f, d, costs)
+    a_p, a_c, b_p, b_c = perms.copy(), costs.copy(), perms.copy(), costs.copy()
+    orc.twoopt_many(a_p, f, d, a_c, 2)
+    batch.twoopt_many(b_p, f, d, b_c, 2)
+    assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c)
