@@ -773,28 +773,62 @@ step_kernel(const StepArgs a) {
         for (int k = 0; k < CPL; ++k) tot2[k] = 0.f;
         // |c1 v| <= v_max guaranteed for every stored v: the clamp is a no-op
         const float vmc = a.v_bounded ? __int_as_float(0x7f800000) : vm;
-        int r = 0;
-        for (; r + 1 < n; r += 2) {
+        if constexpr (G == 1 && CPL == 2) {
+          // n in 33..64: slot 0 is live in every lane; a dead slot 1 re-runs
+          // slot 0's column with a unit factor (same thread, idempotent),
+          // which keeps the loop branch-free.  Running smem pointers.
+          const bool live1 = cfree[1];
+          float* q0 = reinterpret_cast<float*>(tile) + col[0];
+          float* q1 = reinterpret_cast<float*>(tile) + (live1 ? col[1] : col[0]);
+          const float f1 = live1 ? c1f : 1.0f;
+          const int n2 = 2 * n;
+          auto run = [&](auto clampit) {
+            auto cl = [&](float x) -> float {
+              if constexpr (decltype(clampit)::value) return fminf(fmaxf(x, -vmc), vmc);
+              else return x;
+            };
+            int r = 0;
+            for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+              const float a0 = cl(c1f * q0[0]), a1 = cl(c1f * q0[n]);
+              q0[0] = a0; q0[n] = a1;
+              tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
+              const float b0 = cl(f1 * q1[0]), b1 = cl(f1 * q1[n]);
+              q1[0] = b0; q1[n] = b1;
+              tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
+            }
+            if (r < n) {
+              const float a0 = cl(c1f * q0[0]);
+              q0[0] = a0; tot[0] += fabsf(a0);
+              const float b0 = cl(f1 * q1[0]);
+              q1[0] = b0; tot[1] += fabsf(b0);
+            }
+          };
+          if (a.v_bounded) run(std::false_type{});
+          else run(std::true_type{});
+        } else {
+          int r = 0;
+          for (; r + 1 < n; r += 2) {
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            if (!cfree[k]) continue;
-            float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-            const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
-            const float l1 = fminf(fmaxf(c1f * cell[n], -vmc), vmc);
-            cell[0] = l0;
-            cell[n] = l1;
-            tot[k] += fabsf(l0);
-            tot2[k] += fabsf(l1);
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+              const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
+              const float l1 = fminf(fmaxf(c1f * cell[n], -vmc), vmc);
+              cell[0] = l0;
+              cell[n] = l1;
+              tot[k] += fabsf(l0);
+              tot2[k] += fabsf(l1);
+            }
           }
-        }
-        if (r < n) {
+          if (r < n) {
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            if (!cfree[k]) continue;
-            float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-            const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
-            cell[0] = l0;
-            tot[k] += fabsf(l0);
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+              const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
+              cell[0] = l0;
+              tot[k] += fabsf(l0);
+            }
           }
         }
 #pragma unroll
@@ -857,6 +891,61 @@ step_kernel(const StepArgs a) {
         m = gt ? w : m;
       };
       auto stats_rows = [&](auto do_scale) {
+        if constexpr (G == 1 && CPL == 2) {
+          // branch-free form (see the velocity loop): a dead slot 1 rescans
+          // slot 0's column with a unit factor; its statistics are unused
+          const bool live1 = cfree[1];
+          VT* q0 = tile + col[0];
+          VT* q1 = tile + (live1 ? col[1] : col[0]);
+          const VT s0 = inv[0], s1 = live1 ? inv[1] : (VT)1;
+          // the z cells are parked at -inf during the scan (restored below),
+          // so the loop needs no per-row z test
+          VT* zp0 = q0 + zr[0] * n;
+          VT* zp1 = q1 + (live1 ? zr[1] : zr[0]) * n;
+          const VT zv0 = *zp0;
+          const VT zv1 = live1 ? *zp1 : (VT)0;
+          *zp0 = NINF;
+          if (live1) *zp1 = NINF;
+          const int z0 = -1, z1 = -1;
+          const int n2 = 2 * n;
+          auto sc_ = [&](VT v, VT f, int k) -> VT {
+            if constexpr (sizeof(VT) == 8) return k == 0 || live1 ? __ddiv_rn(v, total[k]) : v;
+            else return v * f;
+          };
+          auto upd2 = [&](VT w, int r, int, VT& m, int& c, int& rr) {
+            const bool gt = w > m;
+            c = gt ? 1 : c + (w == m ? 1 : 0);
+            rr = gt ? r : rr;
+            m = gt ? w : m;
+          };
+          int r = 0;
+          for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+            VT a0 = q0[0], a1 = q0[n];
+            if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); a1 = sc_(a1, s0, 0); q0[0] = a0; q0[n] = a1; }
+            upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
+            upd2(a1, r + 1, z0, mB[0], cB[0], rB[0]);
+            VT b0 = q1[0], b1 = q1[n];
+            if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); b1 = sc_(b1, s1, 1); q1[0] = b0; q1[n] = b1; }
+            upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
+            upd2(b1, r + 1, z1, mB[1], cB[1], rB[1]);
+          }
+          if (r < n) {
+            VT a0 = q0[0];
+            if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); q0[0] = a0; }
+            upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
+            VT b0 = q1[0];
+            if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); q1[0] = b0; }
+            upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
+          }
+          if constexpr (decltype(do_scale)::value) {
+            *zp0 = sc_(zv0, s0, 0);
+            if (live1) *zp1 = sc_(zv1, s1, 1);
+          } else {
+            *zp0 = zv0;
+            if (live1) *zp1 = zv1;
+          }
+          return;
+        }
         int r = 0;
         for (; r + 1 < n; r += 2) {
 #pragma unroll
