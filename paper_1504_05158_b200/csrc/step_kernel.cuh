@@ -660,16 +660,27 @@ step_kernel(const StepArgs a) {
     }
   };
   int64_t p = a.work ? bcast(claim()) : (int64_t)blockIdx.x * W + gidx;
+  // The next particle's tile is prefetched as soon as the aggregation has
+  // stopped reading the current one, so the load overlaps the goal and
+  // personal-best phases; `loaded` says whether p's load is in flight.
+  bool loaded = false;
+  auto issue_load = [&](int64_t pp) {
+    if (tid == 0) {
+      bulk_wait_read();                 // the previous bulk store has left the tile
+      mbar_arrive_expect_tx(&sc.bar, tile_bytes);
+      bulk_load(tile, reinterpret_cast<VT*>(a.V) + pp * a.vstride, tile_bytes, &sc.bar);
+    }
+  };
   while (p < a.P) {
     const unsigned q_next = a.work ? claim() : 0u;
+    int64_t p_next = -1;
     VT* gV = reinterpret_cast<VT*>(a.V) + p * a.vstride;
     if constexpr (GT) {
       tile = gV;
-    } else if (tid == 0) {
-      bulk_wait_read();                 // previous particle's store has left the tile
-      mbar_arrive_expect_tx(&sc.bar, tile_bytes);
-      bulk_load(tile, gV, tile_bytes, &sc.bar);
+    } else if (!loaded) {
+      issue_load(p);
     }
+    loaded = false;
 
     QSB_COUNT(0, 1);
     DrawRow dr;
@@ -1373,6 +1384,11 @@ step_kernel(const StepArgs a) {
         }
       }
       Sync::sync();
+      if constexpr (!GT) {
+        // the tile is no longer read for this particle: prefetch the next one
+        p_next = a.work ? bcast(q_next) : p + ngroups;
+        if (p_next < a.P) { issue_load(p_next); loaded = true; }
+      }
       int16_t* gnew = a.perm_new + p * n;
       #pragma unroll 1
       for (int c = tid; c < n; c += NT) gnew[c] = (int16_t)sc.sperm[c];
@@ -1465,7 +1481,8 @@ step_kernel(const StepArgs a) {
       }
     }
     Sync::sync();
-    p = a.work ? bcast(q_next) : p + ngroups;
+    if (p_next < 0) p_next = a.work ? bcast(q_next) : p + ngroups;
+    p = p_next;
   }
   if (!GT && tid == 0) bulk_wait_all();
 }
