@@ -16,6 +16,7 @@ from .engine import (
     RunResult,
     init_population,
     step,
+    step_many,
     run,
     projected_buffer_bytes,
     device_buffer_bytes,
@@ -31,6 +32,6 @@ __all__ = [
     "QapInstance", "parse_instance", "load_instance", "taillard_uniform",
     "SwarmBestTable", "MigrationEvent", "migrate",
     "IterationStats", "percentile", "pmf", "collect", "export_csv", "write_solution",
-    "PopulationState", "RunResult", "init_population", "step", "run",
+    "PopulationState", "RunResult", "init_population", "step", "step_many", "run",
     "projected_buffer_bytes", "device_buffer_bytes", "gap", "batch", "collect_device",
 ]

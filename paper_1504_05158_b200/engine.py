@@ -542,6 +542,109 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     return state
 
 
+def _due_epochs(config: SolverConfig, t0: int, t1: int) -> int:
+    """Migration events in iterations t0+1 .. t1."""
+    if config.migration_factor <= 0.0 or config.migration_depth <= 0:
+        return 0
+    P = config.migration_period
+    return t1 // P - t0 // P
+
+
+def step_many(state: PopulationState, instance, config: SolverConfig, steps: int) -> PopulationState:
+    """Advance ``steps`` iterations, replaying one CUDA graph that holds two
+    iterations (so perm / perm_new return to their buffers) with migration
+    decided on the device (t % migration_period).  Results are identical to
+    calling :func:`step` ``steps`` times; the host only launches the graph.
+    Single-device states only."""
+    if steps <= 0:
+        return state
+    if state.local_particles != state.num_particles:
+        raise ValueError("step_many drives single-device states; use step() with an exchange")
+    # one eager iteration fixes the launch hints (bounded velocity, current costs)
+    step(state, instance, config)
+    steps -= 1
+    pairs = steps // 2
+    if pairs >= 2:
+        rt = _runtime(state, instance, config)
+        t0 = state.t
+        d = config.migration_depth if config.migration_factor > 0.0 else 0
+        mig = None
+        # a captured graph without migration is reusable while the buffers line up
+        key = (rt.key, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr())
+        cached = getattr(state, "_graph_cache", None)
+        if d == 0 and cached is not None and cached[0] == key:
+            graph = cached[1]
+            for _ in range(pairs):
+                graph.replay()
+            passes = config.two_opt_passes
+            state.launches += pairs * 2 * (2 + (1 if passes else 0))
+            state.t = t0 + 2 * pairs
+            state._host_best = None
+            for _ in range(steps - 2 * pairs):
+                step(state, instance, config)
+            return state
+        if d > 0:
+            _drain_log(state)
+            ms = _MigrationScratch(state, d)
+            epochs = _due_epochs(config, t0, t0 + 2 * pairs)
+            ms.log = torch.zeros((max(epochs, 1), d, 6), dtype=torch.float64, device=state.device)
+            e0 = (t0 + 1 + config.migration_period - 1) // config.migration_period
+            rows = max(1, (t0 + 2 * pairs) // config.migration_period - e0 + 1)
+            tab = np.stack([migration_picks(config.seed, (e0 + r) * config.migration_period, d,
+                                            state.swarm_size) for r in range(rows)])
+            ms.picks = torch.from_numpy(tab).to(state.device)
+            ms.e0, ms.rows = e0, rows
+            state._mig = ms
+            mig = _lib.QsbMigration()
+            mig.d, mig.period, mig.mode, mig.reserved = d, config.migration_period, 0, 0
+            mig.num_swarms_total = state.swarms
+            mig.picks, mig.picks_epoch0, mig.picks_rows = ms.picks.data_ptr(), ms.e0, ms.rows
+            mig.all_pg_cost = state.d_pg_cost.data_ptr()
+            mig.plan, mig.records = ms.plan.data_ptr(), ms.records.data_ptr()
+            mig.log, mig.log_rows = ms.log.data_ptr(), ms.log.shape[0]
+            mig.log_count = ms.log_count.data_ptr()
+            mig.status = ms.status.data_ptr()
+        passes = config.two_opt_passes
+        flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
+        tf = _lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+        cs_a = state.c_state()
+        cs_b = _lib.QsbState.from_buffer_copy(cs_a)
+        cs_b.perm, cs_b.perm_new = cs_a.perm_new, cs_a.perm
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(state.device)
+        side.wait_stream(torch.cuda.current_stream(state.device))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                s = side.cuda_stream
+                for cs in (cs_a, cs_b):
+                    _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, flags, None, 0, 2, None, 0, s)
+                    if passes:
+                        _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, s)
+                    _lib.call("qsb_best_update", cs, s)
+                    if mig is not None:
+                        mst = _lib.QsbState.from_buffer_copy(cs)
+                        mst.perm = cs.perm_new           # migration reads the post-swap positions
+                        _lib.call("qsb_migrate", mst, mig, s)
+        torch.cuda.current_stream(state.device).wait_stream(side)
+        for _ in range(pairs):
+            graph.replay()
+        torch.cuda.current_stream(state.device).wait_stream(side)
+        state.launches += pairs * 2 * (2 + (1 if passes else 0))
+        state.t = t0 + 2 * pairs
+        if mig is not None:
+            state._mig.pending = _due_epochs(config, t0, t0 + 2 * pairs)
+            _drain_log(state)
+            state._mig = None          # later eager steps get a standard scratch
+        state._host_best = None
+        steps -= 2 * pairs
+        state._graph_keepalive = graph
+        if mig is None:
+            state._graph_cache = (key, graph)
+    for _ in range(steps):
+        step(state, instance, config)
+    return state
+
+
 @dataclass
 class RunResult:
     """Outcome of a full run plus the collected statistics (engine.py:247-265)."""
@@ -581,7 +684,10 @@ def run(config: SolverConfig, instance, collect_stats: bool = True, device=None)
         series.append(collect_device(state, 1000.0 * (time.perf_counter() - t_start),
                                      bins=config.pmf_bins,
                                      all_swarms=config.record_all_swarm_percentiles))
-    for _ in range(config.max_iterations):
+    if not collect_stats and config.target_cost is None:
+        # nothing is read back per iteration: replay CUDA graphs
+        step_many(state, instance, config, config.max_iterations)
+    for _ in range(config.max_iterations if (collect_stats or config.target_cost is not None) else 0):
         if config.target_cost is not None and state.best_cost <= config.target_cost:
             break
         it_start = time.perf_counter()

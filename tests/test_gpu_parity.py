@@ -340,3 +340,41 @@ def test_twoopt_large_symmetric_vs_oracle(n):
     orc.twoopt_many(a_p, f, d, a_c, 2)
     batch.twoopt_many(b_p, f, d, b_c, 2)
     assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c)
+
+
+# ------------------------------------------------------------- CUDA graphs
+@pytest.mark.parametrize("kw", [dict(migration_factor=0.3, migration_period=1),
+                                dict(migration_factor=0.3, migration_period=3),
+                                dict(two_opt_passes=1), dict(precision="fp32", migration_factor=0.25,
+                                                             migration_period=2)])
+def test_step_many_graph_equals_eager_steps(kw, golden_instances):
+    inst = golden_instances["tai30"]
+    base = dict(swarms=6, swarm_size=10, seed=9, coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    base.update(kw)
+    cfg = qsb.SolverConfig(**base)
+    a = qsb.init_population(cfg, inst)
+    b = qsb.init_population(cfg, inst)
+    for _ in range(13):
+        qsb.step(a, inst, cfg)
+    qsb.step_many(b, inst, cfg, 13)
+    assert a.t == b.t == 13
+    assert digest(a) == digest(b)
+    assert (a.best_cost, a.best_iteration) == (b.best_cost, b.best_iteration)
+    assert [tuple(e) for e in a.migration_log] == [tuple(e) for e in b.migration_log]
+    # eager steps after a graph segment keep working
+    qsb.step(a, inst, cfg)
+    qsb.step(b, inst, cfg)
+    assert digest(a) == digest(b)
+
+
+def test_run_without_stats_uses_graphs_and_matches(golden_instances):
+    inst = golden_instances["chr12a"]
+    cfg = qsb.SolverConfig(swarms=10, swarm_size=20, seed=3, max_iterations=40,
+                           migration_factor=0.2, coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    r1 = qsb.run(cfg, inst, collect_stats=False)
+    st = qsb.init_population(cfg, inst)
+    for _ in range(40):
+        qsb.step(st, inst, cfg)
+    assert (r1.best_cost, r1.best_iteration, r1.iterations_run) == (st.best_cost, st.best_iteration, 40)
+    assert r1.best_perm.tolist() == st.best_perm.tolist()
+    assert [tuple(e) for e in r1.migration_events] == [tuple(e) for e in st.migration_log]
