@@ -90,6 +90,16 @@ typedef struct qsb_state {
   int64_t* swarm_min_idx;    /* (m,) scratch */
   uint32_t* done;            /* (1,) scratch, zero-initialised */
   uint32_t* work;            /* (1,) scratch for dynamic particle scheduling, or NULL */
+  /* Lazily scaled fp32 layout (optional; NULL = V holds v itself).  When set
+   * (v_dtype QSB_F32, n <= 64), V holds u and the velocity is v = u * s
+   * per column; vcol is (P, 5, vcs) 32-bit words with vcs = n rounded up to
+   * a multiple of 4: row 0 the column scale s (f32), rows 1-2 the low / high
+   * words of the f64 sum of |u| over the column, row 3 the maximum of u over
+   * the rows other than zp (f32, NaN = unknown), row 4 (int32) count << 16 |
+   * first row << 8 | zp, zp being the z row (the position) of the step that
+   * wrote them.  Set row 0 to 1 and row 3 to NaN whenever V is written from
+   * outside the step. */
+  float* vcol;
 } qsb_state;
 
 /* QAP instance on the device (qaplib.QapInstance, qaplib.py:28-69). */

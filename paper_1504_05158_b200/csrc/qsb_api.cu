@@ -169,10 +169,10 @@ int qsb_last_cuda_error(void) { return g_last_cuda; }
 
 #ifdef QSB_COUNTERS
 // diagnosis builds only: read and reset the step-kernel event counters
-int qsb_debug_counters(unsigned long long* out8) {
-  cudaError_t e = cudaMemcpyFromSymbol(out8, qsb_counters, 8 * sizeof(unsigned long long));
+int qsb_debug_counters(unsigned long long* out12) {
+  cudaError_t e = cudaMemcpyFromSymbol(out12, qsb_counters, 12 * sizeof(unsigned long long));
   if (e != cudaSuccess) return cuda_status(e);
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   return cuda_status(cudaMemcpyToSymbol(qsb_counters, z, sizeof(z)));
 }
 #endif
@@ -211,6 +211,8 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.acc32 = inst ? inst->acc32 : 0;
   a.v_bounded = (co->hints & QSB_HINT_V_BOUNDED) ? 1 : 0;
   a.cost_incremental = (co->hints & QSB_HINT_COST_CURRENT) ? 1 : 0;
+  a.vcol = st->v_dtype == QSB_F32 ? st->vcol : nullptr;
+  a.vcstride = (st->n + 3) / 4 * 4;
 }
 
 int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co,

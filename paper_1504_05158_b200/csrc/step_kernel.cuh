@@ -71,6 +71,8 @@ struct StepArgs {
   int acc32;                 // host guarantee: n * max(F) * max(D) < 2^32
   int cost_incremental;      // host guarantee: cost[p] == goal(perm[p]) on entry
   unsigned int* work;        // optional zeroed counter: dynamic particle scheduling
+  float* vcol;               // fp32 lazily scaled layout: (P, 4, vcstride) column state, or null
+  int vcstride;
 };
 
 struct Best {
@@ -148,22 +150,28 @@ __device__ __forceinline__ int nth_set_bit32(unsigned m, int k) {
   return pos;
 }
 
-// Per-group shared scratch (one per particle group in the CTA).
+// Per-group shared scratch (one per particle group in the CTA).  Row and
+// column indices are < 256, so the per-column arrays are bytes (this keeps
+// four one-warp CTAs of four particles resident per SM at n = 50).
 template <int NMAX, int G>
 struct GroupScratch {
-  int sperm[NMAX];     // perm_new under construction (aggregation output)
-  int szr[NMAX];       // perm of the current position X (z row per column)
-  int srow[NMAX];      // per-row tie counts / pick-column match flags / lists
-  int sorder[NMAX];    // pick-column visiting order
-  unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
-  uint64_t sbulk[NMAX];      // z keys assigned by bulk steps (pending tie-draw count)
-  uint64_t tmask[NMAX];      // per tied column: mask of tied rows (one-warp tie path)
+  union {
+    uint64_t sbulk[NMAX];    // z keys assigned by bulk steps (pending tie-draw count)
+    uint64_t tmask[NMAX];    // per tied column: mask of tied rows (one-warp tie path;
+                             // used only after the pending bulk keys were counted)
+  };
   unsigned long long rmw[(NMAX + 63) / 64];   // rows retired by a bulk step (multi-warp groups)
-  Best slots[2][G];
-  int islots[2][G];
-  int64_t lslots[G];
-  int ssel[4];
   uint64_t bar;
+  Best slots[2][G];
+  int64_t lslots[G];
+  int islots[2][G];
+  int ssel[4];
+  float sS[NMAX];        // column scales of the fp32 tile (lazily scaled layout; else 1)
+  uint16_t srow[NMAX];   // per-row tie counts / pick-column match flags / lists
+  uint8_t sperm[NMAX];   // perm_new under construction (aggregation output)
+  uint8_t szr[NMAX];     // perm of the current position X (z row per column)
+  uint8_t sorder[NMAX];  // pick-column visiting order
+  unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
 };
 
 template <int G>
@@ -175,9 +183,10 @@ struct GroupSync {
 
 // Optional event counters for diagnosis builds (-DQSB_COUNTERS): particles,
 // normal rounds, bulk steps, bulk z cells, tie rounds, warp tie paths,
-// slow tie paths, rescans.
+// slow tie paths, rescans; lazily scaled layout: full passes, incremental
+// rescans, rescans with unknown column state.
 #ifdef QSB_COUNTERS
-__device__ unsigned long long qsb_counters[8];
+__device__ unsigned long long qsb_counters[12];
 #define QSB_COUNT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&qsb_counters[i], (unsigned long long)(v)); } while (0)
 #else
 #define QSB_COUNT(i, v) do { } while (0)
@@ -238,13 +247,21 @@ __device__ __forceinline__ int group_min_int(int x, Scratch& sc, int& ipar, int 
   return x;
 }
 
+// Velocity value of a stored entry.  fp64 tiles hold v itself; fp32 tiles
+// hold u with v = u * s (s the column scale of the lazily scaled layout, 1.0
+// otherwise), and the product is exact in double.
 template <typename VT>
-__device__ __forceinline__ uint64_t nonz_key(VT v) {   // key of m = 0.0 + v
-  return okey(__dadd_rn(0.0, (double)v));
+__device__ __forceinline__ double vval(VT u, float s) {
+  if constexpr (sizeof(VT) == 8) return u;
+  else return (double)u * (double)s;
 }
 template <typename VT>
-__device__ __forceinline__ uint64_t z_key(VT v) {      // key of m = 1.0 + v
-  return okey(__dadd_rn(1.0, (double)v));
+__device__ __forceinline__ uint64_t nonz_key(VT v, float s) {   // key of m = 0.0 + v
+  return okey(__dadd_rn(0.0, vval(v, s)));
+}
+template <typename VT>
+__device__ __forceinline__ uint64_t z_key(VT v, float s) {      // key of m = 1.0 + v
+  return okey(__dadd_rn(1.0, vval(v, s)));
 }
 
 // Set of free rows (bit r of word r/64).
@@ -261,8 +278,8 @@ struct RowSet {
 };
 
 template <typename VT>
-__device__ __forceinline__ uint64_t mkey(const VT* tile, int n, int r, int c, int zrc) {
-  return okey(cell_m(tile[r * n + c], r == zrc));
+__device__ __forceinline__ uint64_t mkey(const VT* tile, const float* sS, int n, int r, int c, int zrc) {
+  return okey(__dadd_rn(r == zrc ? 1.0 : 0.0, vval(tile[r * n + c], sS[c])));
 }
 
 // ---- rare paths, kept out of line so the round loop stays in I-cache ----
@@ -298,7 +315,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
         if (!tf) continue;
         const int zc = sc.szr[c];
         if (r == zc && tf != 2) continue;
-        if (mkey(tile, n, r, c, zc) == key) ++cnt;
+        if (mkey(tile, sc.sS, n, r, c, zc) == key) ++cnt;
       }
     }
     sc.srow[r] = cnt;
@@ -313,7 +330,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
       if (!tf) continue;
       const int zc = sc.szr[c];
       if (r == zc && tf != 2) continue;
-      if (mkey(tile, n, r, c, zc) == key) {
+      if (mkey(tile, sc.sS, n, r, c, zc) == key) {
         if (q == 0) { cc = c; break; }
         --q;
       }
@@ -332,7 +349,7 @@ __device__ __noinline__ int first_row_scan(const VT* tile, int n, Scratch& sc, R
   const int zc = sc.szr[c];
   int found = INT_MAX;
   for (int r = tid; r < n; r += NT)
-    if (rf.has(r) && (r != zc || zok) && mkey(tile, n, r, c, zc) == key) found = min(found, r);
+    if (rf.has(r) && (r != zc || zok) && mkey(tile, sc.sS, n, r, c, zc) == key) found = min(found, r);
   return group_min_sync<G>(found, sc, lane, tid);
 }
 
@@ -405,8 +422,8 @@ __device__ __noinline__ int tie_select_warp(const VT* tile, int n, Scratch& sc, 
       b &= b - 1;
       const int zc = sc.szr[c];
       const bool zok = sc.stie[c] == 2;
-      const bool a0 = r0ok && (c0 != zc || zok) && mkey(tile, n, c0, c, zc) == key;
-      const bool a1 = r1ok && (c1 != zc || zok) && mkey(tile, n, c1, c, zc) == key;
+      const bool a0 = r0ok && (c0 != zc || zok) && mkey(tile, sc.sS, n, c0, c, zc) == key;
+      const bool a1 = r1ok && (c1 != zc || zok) && mkey(tile, sc.sS, n, c1, c, zc) == key;
       const unsigned m0 = __ballot_sync(FULL, a0), m1 = __ballot_sync(FULL, a1);
       cnt0 += a0;
       cnt1 += a1;
@@ -467,7 +484,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
     Best rb = best_none();
     for (int r = tid; r < n; r += NT) {
       if (!rf.has(r)) continue;
-      const uint64_t key = mkey(tile, n, r, c, zc);
+      const uint64_t key = mkey(tile, sc.sS, n, r, c, zc);
       if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
       else if (key == rb.key) ++rb.cnt;
     }
@@ -478,7 +495,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
       const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
       const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
       for (int r = tid; r < n; r += NT)
-        sc.srow[r] = (rf.has(r) && mkey(tile, n, r, c, zc) == b.key) ? 1 : 0;
+        sc.srow[r] = (rf.has(r) && mkey(tile, sc.sS, n, r, c, zc) == b.key) ? 1 : 0;
       GroupSync<G>::sync();
       if (tid == 0) {
         int q = pick, r = 0;
@@ -597,6 +614,11 @@ step_kernel(const StepArgs a) {
   using Scratch = typename K::Scratch;
   using Sync = GroupSync<G>;
   constexpr bool kFloatMat = std::is_floating_point<MT>::value;
+  // Lazily scaled fp32 layout (a.vcol set; one-warp groups): the tile holds
+  // u with v = u * s per column, and a step rewrites only the <= 3 entries
+  // per column that x / pl / pg touch ("lazy column scale").
+  constexpr bool kLazy = sizeof(VT) == 4 && G == 1 && !GT;
+  const bool lazy = kLazy && a.vcol != nullptr;
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
@@ -629,7 +651,7 @@ step_kernel(const StepArgs a) {
     }
   }
   if (tid == 0) { mbar_init(&sc.bar, 1); mbar_fence_init(); }
-  for (int c = tid; c < K::NMAX; c += NT) sc.stie[c] = 0;
+  for (int c = tid; c < K::NMAX; c += NT) { sc.stie[c] = 0; sc.sS[c] = 1.0f; }
   __syncthreads();
 
   const uint64_t t = a.t_dev ? (uint64_t)(*a.t_dev) + 1 : a.t_host;
@@ -707,6 +729,42 @@ step_kernel(const StepArgs a) {
         pgr[k] = a.pg_perm[s * n + col[k]];
       }
     }
+    // lazily scaled layout: column scale s, sum A of |u| over the column,
+    // and the max / tie count / first row of u over the rows other than the
+    // z row zp of the step that wrote them (M = NaN: not known)
+    float cs[CPL], cM[CPL];
+    double cA[CPL];
+    int cCR[CPL];
+    const int vcs = a.vcstride;
+    float* vcp = lazy ? a.vcol + p * 5 * (int64_t)vcs : nullptr;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      cs[k] = 1.0f; cA[k] = 0.0; cM[k] = 0.0f; cCR[k] = 0;
+      if (lazy && cfree[k]) {
+        cs[k] = vcp[col[k]];
+        cA[k] = __hiloint2double(__float_as_int(vcp[2 * vcs + col[k]]),
+                                 __float_as_int(vcp[vcs + col[k]]));
+        cM[k] = vcp[3 * vcs + col[k]];
+        cCR[k] = __float_as_int(vcp[4 * vcs + col[k]]);
+      }
+    }
+    // incremental step: every column's state known and in range, no clamp
+    // on the untouched entries, c1 > 0 (else the full pass, which also
+    // renormalises: u := v, s := 1 / sum |v|)
+    bool incr = false;
+    if (lazy && do_vel) {
+      bool ok = a.v_bounded && a.c1 > 0.0;
+      const float c1f = (float)a.c1;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        const float c1s = c1f * cs[k];
+        ok &= cM[k] == cM[k] && cs[k] >= 0x1p-60f && cs[k] <= 0x1p60f && c1s >= 0x1p-100f &&
+              c1s <= 0x1p100f;
+      }
+      incr = __all_sync(FULL, ok);
+      if (!incr) QSB_COUNT(8, 1);
+    }
     double c2r2 = 0.0, c3r3 = 0.0;
     if (do_vel) {
       if (a.coef) { c2r2 = a.coef[2 * p]; c3r3 = a.coef[2 * p + 1]; }
@@ -760,12 +818,76 @@ step_kernel(const StepArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < CPL; ++k) total[k] = (VT)tot[k];
+      } else if (incr) {
+        // lazily scaled layout, incremental: v' = normalise(c1 v + ...) is
+        // c1 s u / total on every entry x / pl / pg leave alone, so those
+        // keep u and the column scale becomes s' = c1 s / total; the
+        // touched entries get u' = lin / (c1 s).  Since total = c1 s A' with
+        // A' = sum |u'|, s' = 1 / A'.  The all-rows statistics are updated
+        // entry by entry (an entry leaving the maximum forces a rescan).
+        const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
+        const float vm = (float)a.vmax;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!cfree[k]) continue;
+          const int xr = zr[k], lr = plr[k], gr = pgr[k], c = col[k];
+          // the touched entries are computed in double: pulls and the
+          // inertia term can cancel, and u' = lin / (c1 s) is rounded once
+          const double c1sd = a.c1 * (double)cs[k];
+          double rcd = (double)(1.0f / (float)c1sd);
+          rcd = rcd * (2.0 - c1sd * rcd);
+          rcd = rcd * (2.0 - c1sd * rcd);
+          // statistics over the rows other than zp (the previous step's z row)
+          float M = cM[k];
+          int cnt = cCR[k] >> 16, R = (cCR[k] >> 8) & 0xff;
+          const int zp = cCR[k] & 0xff;
+          double Ad = cA[k];
+          bool bad = false;
+          float* colp = reinterpret_cast<float*>(tile) + c;
+          auto upd = [&](int r) {
+            const int i2 = (r == lr) - (r == xr), i3 = (r == gr) - (r == xr);
+            if (i2 == 0 && i3 == 0) return;
+            const float u = colp[r * n];
+            const double lin = fmin(fmax(fma(c3r3, (double)i3, fma(c2r2, (double)i2, c1sd * (double)u)),
+                                         -a.vmax), a.vmax);
+            const float u2 = (float)(lin * rcd);
+            colp[r * n] = u2;
+            if (store_v) reinterpret_cast<float*>(gV)[r * n + c] = u2;
+            Ad += (double)fabsf(u2) - (double)fabsf(u);
+            if (r == zp) return;
+            if (u2 > M) { M = u2; cnt = 1; R = r; }
+            else if (u == M) { if (u2 < M && (--cnt == 0 || R == r)) bad = true; }
+            else if (u2 == M) { ++cnt; R = min(R, r); }
+          };
+          upd(xr);
+          if (lr != xr) upd(lr);
+          if (gr != xr && gr != lr) upd(gr);
+          if (xr != zp) {
+            // the excluded row moves from zp to this step's z row xr
+            const float uo = colp[zp * n];
+            if (uo > M) { M = uo; cnt = 1; R = zp; }
+            else if (uo == M) { ++cnt; R = min(R, zp); }
+            if (colp[xr * n] == M && (--cnt == 0 || R == xr)) bad = true;
+          }
+          // A' is kept in double (exact differences of fp32 values); a
+          // column that shrinks sharply is re-summed
+          bad |= !(Ad >= 0.0625 * cA[k]);
+          cA[k] = Ad;
+          cM[k] = M;
+          cCR[k] = bad ? -1 : ((cnt << 16) | (R << 8) | xr);
+          total[k] = (float)c1sd;   // incremental mode: total carries the column factor c1 * s
+        }
+        fence_proxy_async_smem();   // generic tile writes before the next bulk load
       } else {
         // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
         // x / pl / pg are patched afterwards (sum order is not significant
-        // under the fp32 tolerance)
+        // under the fp32 tolerance).  Lazily scaled layout: v = u * s, the
+        // column factor is c1 * s and the result stays unnormalised (u' = lin).
         const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
         const float vm = (float)a.vmax;
+        float c1k[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) c1k[k] = c1f * cs[k];
         float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
@@ -791,7 +913,8 @@ step_kernel(const StepArgs a) {
           const bool live1 = cfree[1];
           float* q0 = reinterpret_cast<float*>(tile) + col[0];
           float* q1 = reinterpret_cast<float*>(tile) + (live1 ? col[1] : col[0]);
-          const float f1 = live1 ? c1f : 1.0f;
+          const float f0 = c1k[0];
+          const float f1 = live1 ? c1k[1] : 1.0f;
           const int n2 = 2 * n;
           auto run = [&](auto clampit) {
             auto cl = [&](float x) -> float {
@@ -800,7 +923,7 @@ step_kernel(const StepArgs a) {
             };
             int r = 0;
             for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
-              const float a0 = cl(c1f * q0[0]), a1 = cl(c1f * q0[n]);
+              const float a0 = cl(f0 * q0[0]), a1 = cl(f0 * q0[n]);
               q0[0] = a0; q0[n] = a1;
               tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
               const float b0 = cl(f1 * q1[0]), b1 = cl(f1 * q1[n]);
@@ -808,7 +931,7 @@ step_kernel(const StepArgs a) {
               tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
             }
             if (r < n) {
-              const float a0 = cl(c1f * q0[0]);
+              const float a0 = cl(f0 * q0[0]);
               q0[0] = a0; tot[0] += fabsf(a0);
               const float b0 = cl(f1 * q1[0]);
               q1[0] = b0; tot[1] += fabsf(b0);
@@ -823,8 +946,8 @@ step_kernel(const StepArgs a) {
             for (int k = 0; k < CPL; ++k) {
               if (!cfree[k]) continue;
               float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
-              const float l1 = fminf(fmaxf(c1f * cell[n], -vmc), vmc);
+              const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
+              const float l1 = fminf(fmaxf(c1k[k] * cell[n], -vmc), vmc);
               cell[0] = l0;
               cell[n] = l1;
               tot[k] += fabsf(l0);
@@ -836,7 +959,7 @@ step_kernel(const StepArgs a) {
             for (int k = 0; k < CPL; ++k) {
               if (!cfree[k]) continue;
               float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float l0 = fminf(fmaxf(c1f * cell[0], -vmc), vmc);
+              const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
               cell[0] = l0;
               tot[k] += fabsf(l0);
             }
@@ -852,8 +975,10 @@ step_kernel(const StepArgs a) {
           auto fix = [&](int r, float v0) {
             const float d2 = (float)((r == lr) - (r == xr));
             const float d3 = (float)((r == gr) - (r == xr));
-            const float g = fminf(fmaxf(c1f * v0, -vm), vm);
-            const float sp = fminf(fmaxf(fmaf(c3f, d3, fmaf(c2f, d2, c1f * v0)), -vm), vm);
+            const float g = fminf(fmaxf(c1k[k] * v0, -vm), vm);
+            // in double: the pulls and the inertia term can cancel
+            const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, a.c1 * ((double)v0 * (double)cs[k])));
+            const float sp = (float)fmin(fmax(l, -a.vmax), a.vmax);
             colp[r * n] = sp;
             tot[k] += fabsf(sp) - fabsf(g);
           };
@@ -884,7 +1009,75 @@ step_kernel(const StepArgs a) {
       if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
       else return v * inv[k];
     };
-    if (do_agg) {
+    float sK[CPL];   // column scale of the tile after this phase (v = u * sK)
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) sK[k] = 1.0f;
+    bool stats_done = false;
+    if constexpr (kLazy) {
+      if (lazy && do_vel) {
+        // incremental step: the non-z statistics were carried through the
+        // update; rescan the columns where they became unknown.  Full pass:
+        // rescan every column (the sums in double).
+        bool need[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          need[k] = cfree[k] && (!incr || cCR[k] < 0);
+          if (cfree[k] && !need[k]) {
+            nmax[k] = cM[k]; ncnt[k] = cCR[k] >> 16; nrow[k] = (cCR[k] >> 8) & 0xff;
+          }
+        }
+        // cooperative rescans (lanes over rows): non-z max / count / first
+        // row, and the sum of |u| over all rows
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          unsigned mask = __ballot_sync(FULL, need[k]);
+          while (mask) {
+            const int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            QSB_COUNT(9, 1);
+            const int c = src + k * 32;
+            const int zc = __shfl_sync(FULL, zr[k], src);
+            if (__shfl_sync(FULL, cCR[k], src) < 0) QSB_COUNT(10, 1);
+            unsigned km = 0, kc = 0, kr = INT_MAX;
+            double sum = 0.0;
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+              const int r = lane + j * 32;
+              if (r >= n) continue;
+              const float u = (float)tile[r * n + c];
+              sum += (double)fabsf(u);
+              if (r == zc) continue;
+              const unsigned key = okey32(__fadd_rn(u, 0.0f));
+              if (key > km) { km = key; kc = 1; kr = r; }
+              else if (key == km) ++kc;
+            }
+            const unsigned M = __reduce_max_sync(FULL, km);
+            const bool match = km == M && kc > 0;
+            const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
+            const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+            if (lane == src) {
+              ncnt[k] = (int)tot;
+              nrow[k] = tot ? (int)rr : -1;
+              nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
+              cA[k] = sum;
+              cM[k] = (float)nmax[k];
+              cCR[k] = tot ? (((int)tot << 16) | ((int)rr << 8) | zc) : -1;
+            }
+          }
+        }
+        // s' = 1 / A' (normalised: v' = lin / total, total = c1 s A' in the
+        // incremental step, = A' in the full pass); raw mode or a zero
+        // column: no normalisation
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+          sK[k] = (a.normalize && cA[k] > 0.0) ? 1.0f / (float)cA[k] : (incr ? total[k] : 1.0f);
+        stats_done = true;
+      }
+    }
+    if (stats_done) {
+    } else if (do_agg) {
       // Max / tie count / first row over the non-z rows (the z row is masked
       // to -inf; stored values are finite), accumulated separately over even
       // and odd rows (two independent dependency chains) and merged.  A
@@ -986,7 +1179,9 @@ step_kernel(const StepArgs a) {
       bool all_scale = true;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) all_scale &= scale[k] || !cfree[k];
-      if (__all_sync(FULL, all_scale)) {
+      if (kLazy && lazy) {
+        stats_rows(std::false_type{});  // lazily scaled layout: u' = lin stays unscaled
+      } else if (__all_sync(FULL, all_scale)) {
         stats_rows(std::true_type{});   // the normalised (norm mode) hot path
       } else {
         ColIn<VT, CPL> in;
@@ -1005,10 +1200,8 @@ step_kernel(const StepArgs a) {
         // merge the odd-row half (ties: counts add, first row = smaller row)
         if (nmax[k] == NINF || mB[k] > nmax[k]) { nmax[k] = mB[k]; ncnt[k] = cB[k]; nrow[k] = rB[k]; }
         else if (mB[k] == nmax[k] && mB[k] != NINF) { ncnt[k] += cB[k]; nrow[k] = min(nrow[k], rB[k]); }
-        nk64[k] = ncnt[k] ? nonz_key(nmax[k]) : 0;
-        zkey[k] = z_key(tile[zr[k] * n + col[k]]);
       }
-    } else {
+    } else if (!lazy) {
 #pragma unroll 1
       for (int r = 0; r < n; ++r) {
 #pragma unroll
@@ -1016,12 +1209,43 @@ step_kernel(const StepArgs a) {
           if (scale[k]) tile[r * n + col[k]] = rescale(tile[r * n + col[k]], k);
       }
     }
-    if (!GT && do_vel && store_v) {
+    if constexpr (kLazy) {
+      if (lazy) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!cfree[k]) continue;
+          if (!do_vel) sK[k] = cs[k];
+          sc.sS[col[k]] = sK[k];
+        }
+      }
+    }
+    if (do_agg) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        nk64[k] = ncnt[k] ? nonz_key(nmax[k], sK[k]) : 0;
+        zkey[k] = z_key(tile[zr[k] * n + col[k]], sK[k]);
+      }
+    }
+    if (!GT && do_vel && store_v && !incr) {
       fence_proxy_async_smem();
       Sync::sync();
       if (tid == 0) bulk_store(gV, tile, tile_bytes);
     } else {
       Sync::sync();
+    }
+    if constexpr (kLazy) {
+      if (lazy && do_vel && store_v) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!cfree[k]) continue;
+          vcp[col[k]] = sK[k];
+          vcp[vcs + col[k]] = __int_as_float(__double2loint(cA[k]));
+          vcp[2 * vcs + col[k]] = __int_as_float(__double2hiint(cA[k]));
+          vcp[3 * vcs + col[k]] = cCR[k] < 0 ? __int_as_float(0x7fc00000) : cM[k];
+          vcp[4 * vcs + col[k]] = __int_as_float(cCR[k] < 0 ? 0 : cCR[k]);
+        }
+      }
     }
 
     // ================= phase 2: aggregation S_x(X + V)
@@ -1324,7 +1548,7 @@ step_kernel(const StepArgs a) {
                     ncnt[k] = (int)tot;
                     nrow[k] = tot ? (int)rr : -1;
                     nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
-                    nk64[k] = tot ? nonz_key(nmax[k]) : 0;
+                    nk64[k] = tot ? nonz_key(nmax[k], sK[k]) : 0;
                     recompute(k);
                   }
                 } else {
@@ -1333,7 +1557,7 @@ step_kernel(const StepArgs a) {
                   for (int j = 0; j < CPL; ++j) {
                     const int r = lane + j * 32;
                     if (r >= n || r == zc || !rf.has(r)) continue;
-                    const uint64_t key = nonz_key(tile[r * n + c]);
+                    const uint64_t key = nonz_key(tile[r * n + c], 1.0f);
                     if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                     else if (key == rb.key) ++rb.cnt;
                   }
@@ -1364,7 +1588,7 @@ step_kernel(const StepArgs a) {
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
                 if (r >= n || r == zc || !rf.has(r)) continue;
-                const uint64_t key = nonz_key(tile[r * n + c]);
+                const uint64_t key = nonz_key(tile[r * n + c], sc.sS[c]);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
               }

@@ -63,12 +63,20 @@ def projected_buffer_bytes(config: SolverConfig, n: int) -> int:
     return mats + perms + tables + swarm
 
 
+_LAZY_MAX_N = 64      # one-warp kernel variants carry the lazily scaled layout
+
+
+def _vcs(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
 def device_buffer_bytes(config: SolverConfig, n: int) -> int:
     """HBM bytes of this engine's state for one device holding every particle."""
     p = config.num_particles
     sv = 8 if config.precision == "fp64" else 4
     vstride = -(-n * n // (16 // sv)) * (16 // sv)
-    return p * (vstride * sv + 3 * n * 2 + 2 * 8 + 1) + config.swarms * (n * 2 + 3 * 8)
+    vcol = 20 * _vcs(n) if (sv == 4 and n <= _LAZY_MAX_N) else 0
+    return p * (vstride * sv + vcol + 3 * n * 2 + 2 * 8 + 1) + config.swarms * (n * 2 + 3 * 8)
 
 
 def _dev(device):
@@ -140,6 +148,12 @@ class PopulationState:
             self.d_swarm_min_idx = torch.zeros(self.local_swarms, dtype=torch.int64, **z)
             self.d_done = torch.zeros(1, dtype=torch.int32, **z)
             self.d_work = torch.zeros(1, dtype=torch.int32, **z)
+            # lazily scaled fp32 layout (one-warp kernel variants, n <= 64):
+            # V holds u, v = u * s per column; see include/qapswarm_b200.h
+            self.d_vcol = None
+            if self.v_code == _lib.F32 and n <= _LAZY_MAX_N:
+                self.d_vcol = torch.empty((p, 5, _vcs(n)), dtype=torch.float32, **z)
+                self.reset_vcol()
         except torch.OutOfMemoryError:
             raise MemoryError(
                 f"cannot allocate population buffers: {p} particles of size {n}x{n} need about "
@@ -171,7 +185,7 @@ class PopulationState:
         s.swarm_offset = self.swarm_offset
         for name in ("V", "perm", "perm_new", "pl_perm", "cost", "pl_cost", "improved",
                      "pg_perm", "pg_cost", "best_perm", "best_cost", "best_iter", "best_idx",
-                     "swarm_min", "swarm_min_idx", "done", "work"):
+                     "swarm_min", "swarm_min_idx", "done", "work", "vcol"):
             setattr(s, name, _ptr(getattr(self, "d_" + name)))
         s.iteration = _ptr(self.d_iteration)
         self._cs = s
@@ -212,10 +226,40 @@ class PopulationState:
     def PL(self):
         return self._mats(self.d_pl_perm)
 
+    def reset_vcol(self):
+        """Column state of the lazily scaled layout after V was written from
+        outside the step: scale 1, statistics unknown (the next step runs
+        the full pass)."""
+        if self.d_vcol is not None:
+            self.d_vcol[:, 0].fill_(1.0)
+            self.d_vcol[:, 1:3].zero_()
+            self.d_vcol[:, 3].fill_(float("nan"))
+            self.d_vcol[:, 4].zero_()
+
+    def set_lazy_scale(self, enabled: bool):
+        """Switch the fp32 state to (or from) the lazily scaled layout; V is
+        materialised (u * s, rounded to fp32) when leaving it."""
+        if not enabled and self.d_vcol is not None:
+            p, n = self.local_particles, self.n
+            u = self.d_V[:, :n * n].view(p, n, n)
+            u.mul_(self.d_vcol[:, 0, :n].unsqueeze(1))
+            self.d_vcol = None
+        elif enabled and self.d_vcol is None and self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N:
+            self.d_vcol = torch.empty((self.local_particles, 5, _vcs(self.n)), dtype=torch.float32,
+                                      device=self.device)
+            self.reset_vcol()
+        self._cs = None
+        self._graph_cache = None
+
     @property
     def V(self):
-        p, nn = self.local_particles, self.n * self.n
-        return self.d_V[:, :nn].cpu().numpy().reshape(p, self.n, self.n)
+        """Velocities (P, n, n); fp32 states return float64 when lazily
+        scaled (u * s is exact in float64)."""
+        p, n, nn = self.local_particles, self.n, self.n * self.n
+        u = self.d_V[:, :nn].view(p, n, n)
+        if self.d_vcol is not None:
+            return (u.double() * self.d_vcol[:, 0, :n].double().unsqueeze(1)).cpu().numpy()
+        return u.cpu().numpy()
 
     @property
     def perms(self):
@@ -328,6 +372,7 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
     else:
         _lib.call("qsb_init_population_device", state.c_state(), int(config.seed) & (2**64 - 1),
                   float(config.init_velocity_amplitude), stream)
+    state.reset_vcol()
     _lib.call("qsb_cost", state.d_perm.data_ptr(), p, rt.inst, state.d_cost.data_ptr(), stream)
     state.d_pl_perm.copy_(state.d_perm)
     state.d_pl_cost.copy_(state.d_cost)
