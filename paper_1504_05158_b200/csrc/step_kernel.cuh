@@ -1293,6 +1293,54 @@ step_kernel(const StepArgs a) {
             for (int k = 0; k < CPL; ++k)
               if (cfree[k]) { zel[k] = rf.has(zr[k]); recompute(k); }
           }
+          if constexpr (G == 1 && CPL <= 2) {
+            // ---- endgame: with k <= 5 free columns left (after the bulk
+            // step, typically 4), lane l holds cell (R[l / k], C[l % k]) of
+            // the k x k free submatrix, R / C the free rows / columns in
+            // ascending order.  Lane order is row-major, so every remaining
+            // round is one warp max and a tie picks the pick-th set bit of
+            // the tie ballot (_batch.py:155-170).
+            const int kf = n - rnd;
+            if (!restricted && kf <= 5) {
+              const unsigned cb0 = __ballot_sync(FULL, cfree[0]);
+              const unsigned cb1 = CPL == 2 ? __ballot_sync(FULL, cfree[CPL - 1]) : 0u;
+              const int ei = lane / kf, ej = lane - (lane / kf) * kf;
+              bool act = lane < kf * kf;
+              int er = 0, ec = 0;
+              uint64_t ekey = 0;
+              if (act) {
+                const unsigned rl = (unsigned)rf.w[0], rh = (unsigned)(rf.w[0] >> 32);
+                er = ei < __popc(rl) ? nth_set_bit32(rl, ei) : 32 + nth_set_bit32(rh, ei - __popc(rl));
+                ec = ej < __popc(cb0) ? nth_set_bit32(cb0, ej) : 32 + nth_set_bit32(cb1, ej - __popc(cb0));
+                ekey = mkey(tile, sc.sS, n, er, ec, (int)sc.szr[ec]);
+              }
+#pragma unroll 1
+              for (int left = kf; left > 0; --left) {
+                const uint64_t kk = act ? ekey : 0ULL;
+                const unsigned mh = __reduce_max_sync(FULL, (unsigned)(kk >> 32));
+                const unsigned ml = __reduce_max_sync(FULL, (unsigned)(kk >> 32) == mh ? (unsigned)kk : 0u);
+                const uint64_t M = ((uint64_t)mh << 32) | ml;
+                const unsigned tb = __ballot_sync(FULL, act && ekey == M);
+                const int cnt = __popc(tb);
+                int src = __ffs(tb) - 1;
+                if (cnt > 1) {
+                  if (nbulk) {
+                    cursor += nbulk - bulk_distinct(sc, nbulk, lane);
+                    nbulk = 0;
+                  }
+                  const double u = dr.at(cursor++);
+                  const long long pk = (long long)__dmul_rn(u, (double)cnt);
+                  src = nth_set_bit32(tb, (int)(pk >= cnt ? cnt - 1 : pk));
+                  QSB_COUNT(4, 1);
+                }
+                if (lane == src) sc.sperm[ec] = (uint8_t)er;
+                const int si = src / kf;
+                act = act && ei != si && ej != src - si * kf;
+              }
+              __syncwarp();
+              break;
+            }
+          }
           bool need[CPL];
 #pragma unroll
           for (int k = 0; k < CPL; ++k) need[k] = false;
