@@ -712,17 +712,18 @@ step_kernel(const StepArgs a) {
     dr.base = (uint64_t)(a.p0 + p) * (uint64_t)row_w;
     dr.cached = ~0ULL;
 
-    // ---- per-column registers
+    // ---- per-column registers.  Every global load of the particle's
+    // column data is issued first; the draw block (a dependent Philox chain)
+    // runs while they are in flight.
     int zr[CPL], col[CPL], plr[CPL], pgr[CPL];
     bool cfree[CPL];
     const int16_t* gperm = a.perm + p * n;
-    const int64_t s = p / a.S;
+    const int64_t s = (int64_t)((unsigned)p / (unsigned)a.S);   // P < 2^31 (host-checked)
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       col[k] = tid + k * NT;
       cfree[k] = col[k] < n;
       zr[k] = cfree[k] ? (int)gperm[col[k]] : -1;
-      if (cfree[k]) sc.szr[col[k]] = zr[k];
       plr[k] = pgr[k] = -1;
       if (do_vel && cfree[k]) {
         plr[k] = a.pl_perm[p * n + col[k]];
@@ -748,6 +749,17 @@ step_kernel(const StepArgs a) {
         cCR[k] = __float_as_int(vcp[4 * vcs + col[k]]);
       }
     }
+    double c2r2 = 0.0, c3r3 = 0.0;
+    if (do_vel) {
+      if (a.coef) { c2r2 = a.coef[2 * p]; c3r3 = a.coef[2 * p + 1]; }
+      else {
+        c2r2 = __dmul_rn(a.c2, dr.at(0));   // engine.py:198-199: c2 * r2, c3 * r3
+        c3r3 = __dmul_rn(a.c3, dr.at(1));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      if (cfree[k]) sc.szr[col[k]] = zr[k];
     // incremental step: every column's state known and in range, no clamp
     // on the untouched entries, c1 > 0 (else the full pass, which also
     // renormalises: u := v, s := 1 / sum |v|)
@@ -764,14 +776,6 @@ step_kernel(const StepArgs a) {
       }
       incr = __all_sync(FULL, ok);
       if (!incr) QSB_COUNT(8, 1);
-    }
-    double c2r2 = 0.0, c3r3 = 0.0;
-    if (do_vel) {
-      if (a.coef) { c2r2 = a.coef[2 * p]; c3r3 = a.coef[2 * p + 1]; }
-      else {
-        c2r2 = __dmul_rn(a.c2, dr.at(0));   // engine.py:198-199: c2 * r2, c3 * r3
-        c3r3 = __dmul_rn(a.c3, dr.at(1));
-      }
     }
 
     if constexpr (!GT) {
@@ -831,12 +835,10 @@ step_kernel(const StepArgs a) {
         for (int k = 0; k < CPL; ++k) {
           if (!cfree[k]) continue;
           const int xr = zr[k], lr = plr[k], gr = pgr[k], c = col[k];
-          // the touched entries are computed in double: pulls and the
-          // inertia term can cancel, and u' = lin / (c1 s) is rounded once
+          // lin of a touched entry is formed in double (the pulls and the
+          // inertia term can cancel), then rounded once; u' = lin / (c1 s)
           const double c1sd = a.c1 * (double)cs[k];
-          double rcd = (double)(1.0f / (float)c1sd);
-          rcd = rcd * (2.0 - c1sd * rcd);
-          rcd = rcd * (2.0 - c1sd * rcd);
+          const float rc = __frcp_rn((float)c1sd);
           // statistics over the rows other than zp (the previous step's z row)
           float M = cM[k];
           int cnt = cCR[k] >> 16, R = (cCR[k] >> 8) & 0xff;
@@ -848,9 +850,9 @@ step_kernel(const StepArgs a) {
             const int i2 = (r == lr) - (r == xr), i3 = (r == gr) - (r == xr);
             if (i2 == 0 && i3 == 0) return;
             const float u = colp[r * n];
-            const double lin = fmin(fmax(fma(c3r3, (double)i3, fma(c2r2, (double)i2, c1sd * (double)u)),
-                                         -a.vmax), a.vmax);
-            const float u2 = (float)(lin * rcd);
+            const float lin = fminf(fmaxf((float)fma(c3r3, (double)i3, fma(c2r2, (double)i2, c1sd * (double)u)),
+                                          -vm), vm);
+            const float u2 = lin * rc;
             colp[r * n] = u2;
             if (store_v) reinterpret_cast<float*>(gV)[r * n + c] = u2;
             Ad += (double)fabsf(u2) - (double)fabsf(u);
@@ -1565,6 +1567,10 @@ step_kernel(const StepArgs a) {
             }
           }
           if (rnd >= n - 1) break;
+          if constexpr (G == 1 && CPL <= 2) {
+            // the next round is the endgame, which needs no column statistics
+            if (n - (rnd + 1) <= 5 && !(restricted && rnd + 1 < a.depth)) continue;
+          }
 
           // ---- cooperative rescans of columns whose non-z maximum was retired
           if constexpr (G == 1) {
