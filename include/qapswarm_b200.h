@@ -100,6 +100,9 @@ typedef struct qsb_state {
    * wrote them.  Set row 0 to 1 and row 3 to NaN whenever V is written from
    * outside the step. */
   float* vcol;
+  /* (P, 2) scratch for the step's per-particle (c2 * r2, c3 * r3), drawn by a
+   * one-thread-per-particle pre-pass; NULL = drawn inside the step kernel. */
+  double* step_coef;
 } qsb_state;
 
 /* QAP instance on the device (qaplib.QapInstance, qaplib.py:28-69). */

@@ -41,7 +41,7 @@ class QsbState(ctypes.Structure):
         ("pg_perm", _vp), ("pg_cost", _vp),
         ("best_perm", _vp), ("best_cost", _vp), ("best_iter", _vp), ("best_idx", _vp),
         ("iteration", _vp), ("swarm_min", _vp), ("swarm_min_idx", _vp), ("done", _vp),
-        ("work", _vp), ("vcol", _vp),
+        ("work", _vp), ("vcol", _vp), ("step_coef", _vp),
     ]
 
 

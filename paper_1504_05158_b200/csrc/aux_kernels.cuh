@@ -257,6 +257,28 @@ __global__ void draws_kernel(uint64_t seed, uint64_t t, int64_t p0, int64_t P, i
   }
 }
 
+// Per-particle (c2 * r2, c3 * r3) of iteration t (engine.py:198-199; draw
+// columns 0 and 1 of streams.step_draws), one thread per particle, ahead of
+// the step kernel: keeps the dependent Philox chain off the step kernel's
+// per-particle critical path.
+__global__ void coef_kernel(uint64_t seed, const int64_t* t_dev, uint64_t t_host, int64_t p0,
+                            int64_t P, int n, double c2, double c3, double* out) {
+  const uint64_t t = t_dev ? (uint64_t)(*t_dev) + 1 : t_host;
+  const uint64_t word1 = stream_word(2, t);
+  const uint64_t w = 2 + 2 * (uint64_t)n;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = (uint64_t)(p0 + p) * w;
+    const PhiloxBlock b = philox4x64_10((idx >> 2) + 1, seed, word1);
+    const unsigned l = (unsigned)(idx & 3);   // w is even: l is 0 or 2
+    double u0, u1;
+    if (l == 0) { u0 = u64_to_unit(b.v[0]); u1 = u64_to_unit(b.v[1]); }
+    else { u0 = u64_to_unit(b.v[2]); u1 = u64_to_unit(b.v[3]); }
+    out[2 * p] = __dmul_rn(c2, u0);
+    out[2 * p + 1] = __dmul_rn(c3, u1);
+  }
+}
+
 // ------------------------------------------------------ standalone goal
 template <typename MT, typename PT>
 __global__ void cost_kernel(const PT* perms, int64_t P, int n, const MT* F, const MT* D, void* out) {

@@ -231,6 +231,16 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
   a.inj_stride = inj_stride;
   a.agg_base = agg_base;
   a.coef = coef;
+  if (!coef && !inj_draws && (flags & QSB_PHASE_VELOCITY) && st->step_coef && st->num_particles > 0) {
+    // the step's (c2 r2, c3 r3) from a one-thread-per-particle pre-pass
+    const int64_t P = st->num_particles;
+    const int grid = (int)((P + 255) / 256 < 4 * num_sms() ? (P + 255) / 256 : 4 * num_sms());
+    coef_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(co->seed, st->iteration, t_host, st->particle_offset,
+                                                         P, st->n, co->c2, co->c3, st->step_coef);
+    const int rc = launch_status();
+    if (rc) return rc;
+    a.coef = st->step_coef;
+  }
   a.work = st->work;
   if (a.work) {
     cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), (cudaStream_t)stream);

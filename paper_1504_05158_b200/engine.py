@@ -76,7 +76,7 @@ def device_buffer_bytes(config: SolverConfig, n: int) -> int:
     sv = 8 if config.precision == "fp64" else 4
     vstride = -(-n * n // (16 // sv)) * (16 // sv)
     vcol = 20 * _vcs(n) if (sv == 4 and n <= _LAZY_MAX_N) else 0
-    return p * (vstride * sv + vcol + 3 * n * 2 + 2 * 8 + 1) + config.swarms * (n * 2 + 3 * 8)
+    return p * (vstride * sv + vcol + 3 * n * 2 + 2 * 8 + 16 + 1) + config.swarms * (n * 2 + 3 * 8)
 
 
 def _dev(device):
@@ -148,6 +148,7 @@ class PopulationState:
             self.d_swarm_min_idx = torch.zeros(self.local_swarms, dtype=torch.int64, **z)
             self.d_done = torch.zeros(1, dtype=torch.int32, **z)
             self.d_work = torch.zeros(1, dtype=torch.int32, **z)
+            self.d_step_coef = torch.zeros((p, 2), dtype=torch.float64, **z)
             # lazily scaled fp32 layout (one-warp kernel variants, n <= 64):
             # V holds u, v = u * s per column; see include/qapswarm_b200.h
             self.d_vcol = None
@@ -185,7 +186,7 @@ class PopulationState:
         s.swarm_offset = self.swarm_offset
         for name in ("V", "perm", "perm_new", "pl_perm", "cost", "pl_cost", "improved",
                      "pg_perm", "pg_cost", "best_perm", "best_cost", "best_iter", "best_idx",
-                     "swarm_min", "swarm_min_idx", "done", "work", "vcol"):
+                     "swarm_min", "swarm_min_idx", "done", "work", "vcol", "step_coef"):
             setattr(s, name, _ptr(getattr(self, "d_" + name)))
         s.iteration = _ptr(self.d_iteration)
         self._cs = s
@@ -574,7 +575,7 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
         _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, stream)
         state.launches += 1
     _lib.call("qsb_best_update", cs, stream)
-    state.launches += 2
+    state.launches += 3      # draw pre-pass + fused step + best update
     # after S_v every entry is clamped to v_max, or normalised to |v| <= 1
     state.v_bound = (1.0 + 1e-6) if coeffs.sv_mode == "norm" else coeffs.v_max
     state.swap_positions()
@@ -622,7 +623,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
             for _ in range(pairs):
                 graph.replay()
             passes = config.two_opt_passes
-            state.launches += pairs * 2 * (2 + (1 if passes else 0))
+            state.launches += pairs * 2 * (3 + (1 if passes else 0))
             state.t = t0 + 2 * pairs
             state._host_best = None
             for _ in range(steps - 2 * pairs):
@@ -674,7 +675,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
         for _ in range(pairs):
             graph.replay()
         torch.cuda.current_stream(state.device).wait_stream(side)
-        state.launches += pairs * 2 * (2 + (1 if passes else 0))
+        state.launches += pairs * 2 * (3 + (1 if passes else 0))
         state.t = t0 + 2 * pairs
         if mig is not None:
             state._mig.pending = _due_epochs(config, t0, t0 + 2 * pairs)
