@@ -80,11 +80,23 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
 
 template <typename VT, typename MT, bool DRY>
 static int dispatch_n(const StepArgs& a, cudaStream_t s) {
-  if (a.n <= 32) {
-    if constexpr (DRY) return StepKernel<VT, MT, 1, 1, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
-    else return launch_step<VT, MT, 1, 1, 4>(a, s);
-  }
+  // one-warp groups: fp32 tiles run 16 particles per CTA where they fit (one
+  // CTA per SM, F / D staged once per SM), else 8; fp64 tiles 4 per CTA
   if (a.n <= 64) {
+    if constexpr (sizeof(VT) == 4) {
+      if (a.n <= 32) {
+        if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin())
+          return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16>(a, s);
+      } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
+        return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16>(a, s);
+      } else if (StepKernel<VT, MT, 1, 2, 8>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
+        return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 8>(a, s);
+      }
+    }
+    if (a.n <= 32) {
+      if constexpr (DRY) return StepKernel<VT, MT, 1, 1, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
+      else return launch_step<VT, MT, 1, 1, 4>(a, s);
+    }
     if constexpr (DRY) return StepKernel<VT, MT, 1, 2, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
     else return launch_step<VT, MT, 1, 2, 4>(a, s);
   }

@@ -604,7 +604,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const Col
 
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
-__global__ void __launch_bounds__(32 * G * W, (G == 1 ? QSB_MINB : 1))
+__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : 1))
 step_kernel(const StepArgs a) {
   // GT: the particle tile stays in global memory (L1/L2-cached) instead of
   // being staged in smem -- used when an n x n tile exceeds shared memory.
@@ -667,8 +667,12 @@ step_kernel(const StepArgs a) {
   // else a static grid stride.  The next index is claimed when a particle
   // starts, so the atomic's latency is hidden behind the particle's work.
   auto claim = [&]() -> unsigned {
-    unsigned q = 0;
-    if (tid == 0) q = atomicAdd(a.work, 1u);
+    // plain atom (not the compiler's warp-aggregated form, whose broadcast
+    // would wait for the result right here)
+    unsigned q = 0, lid;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(lid));
+    if (lid == 0 && tid < 32)
+      asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(q) : "l"(a.work + (lid >> 5)) : "memory");
     return q;
   };
   auto bcast = [&](unsigned q) -> int64_t {
