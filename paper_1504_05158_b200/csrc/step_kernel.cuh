@@ -209,8 +209,18 @@ struct StepKernel {
   static __host__ __device__ size_t tile_bytes(int vstride) {
     return GT ? 0 : align_up((size_t)vstride * sizeof(VT), 128);
   }
+  // One-warp groups stage the next particle's column data next to its tile
+  // (cp.async / bulk copies issued with the tile prefetch): the lazily
+  // scaled layout's column state (5 x NMAX words), the perm / pl_perm /
+  // pg_perm rows (3 x NMAX int16), (c2 r2, c3 r3) and, double-buffered,
+  // (cost, pl_cost).
+  static constexpr bool STAGE = G == 1 && !GT;
+  static constexpr size_t SCOL = 0, SPERM = 20 * NMAX, SCOEF = SPERM + 6 * NMAX, SCOST = SCOEF + 16;
+  static __host__ __device__ size_t stage_bytes() {
+    return STAGE ? align_up(SCOST + 32, 128) : 0;
+  }
   static __host__ __device__ size_t group_bytes(int vstride) {
-    return tile_bytes(vstride) + align_up(sizeof(Scratch), 128);
+    return tile_bytes(vstride) + stage_bytes() + align_up(sizeof(Scratch), 128);
   }
   static __host__ __device__ size_t smem_bytes(int n, int vstride, bool fd) {
     return (fd ? fd_bytes(n) : 0) + W * group_bytes(vstride);
@@ -602,6 +612,284 @@ __device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const Col
   return o;
 }
 
+// Column statistics (max / tie count / first row over the non-z rows) of a
+// freshly written tile, with the normalisation fused in (smode 1: every live
+// column scaled; 2: per-column, via stats_generic; 0: no scaling, the lazily
+// scaled layout's full pass).  Out of line for the instruction cache (the
+// lazily scaled layout carries these statistics from step to step).
+template <typename VT, int G, int CPL>
+__device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<VT, CPL> in, int smode) {
+  VT nmax[CPL];
+  int ncnt[CPL], nrow[CPL], col[CPL], zr[CPL];
+  bool cfree[CPL];
+  VT total[CPL], inv[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    nmax[k] = (VT)(-INFINITY); ncnt[k] = 0; nrow[k] = -1;
+    col[k] = in.col[k]; zr[k] = in.zr[k]; cfree[k] = in.cfree[k];
+    total[k] = in.total[k]; inv[k] = in.inv[k];
+  }
+  auto rescale = [&](VT v, int k) -> VT {
+    if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
+    else return v * inv[k];
+  };
+  // Max / tie count / first row over the non-z rows (the z row is masked
+  // to -inf; stored values are finite), accumulated separately over even
+  // and odd rows (two independent dependency chains) and merged.  A
+  // half holding only the z row keeps max = -inf and is ignored.
+  const VT NINF = (VT)(-INFINITY);
+  VT mB[CPL];
+  int cB[CPL], rB[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) { mB[k] = NINF; cB[k] = 0; rB[k] = -1; }
+  auto upd = [&](VT v, int r, int k, VT& m, int& c, int& rr) {
+    const VT w = r == zr[k] ? NINF : v;
+    const bool gt = w > m;
+    c = gt ? 1 : c + (w == m ? 1 : 0);
+    rr = gt ? r : rr;
+    m = gt ? w : m;
+  };
+  auto stats_rows = [&](auto do_scale) {
+    if constexpr (G == 1 && CPL == 2) {
+      // branch-free form (see the velocity loop): a dead slot 1 rescans
+      // slot 0's column with a unit factor; its statistics are unused
+      const bool live1 = cfree[1];
+      VT* q0 = tile + col[0];
+      VT* q1 = tile + (live1 ? col[1] : col[0]);
+      const VT s0 = inv[0], s1 = live1 ? inv[1] : (VT)1;
+      // the z cells are parked at -inf during the scan (restored below),
+      // so the loop needs no per-row z test
+      VT* zp0 = q0 + zr[0] * n;
+      VT* zp1 = q1 + (live1 ? zr[1] : zr[0]) * n;
+      const VT zv0 = *zp0;
+      const VT zv1 = live1 ? *zp1 : (VT)0;
+      *zp0 = NINF;
+      if (live1) *zp1 = NINF;
+      const int z0 = -1, z1 = -1;
+      const int n2 = 2 * n;
+      auto sc_ = [&](VT v, VT f, int k) -> VT {
+        if constexpr (sizeof(VT) == 8) return k == 0 || live1 ? __ddiv_rn(v, total[k]) : v;
+        else return v * f;
+      };
+      auto upd2 = [&](VT w, int r, int, VT& m, int& c, int& rr) {
+        const bool gt = w > m;
+        c = gt ? 1 : c + (w == m ? 1 : 0);
+        rr = gt ? r : rr;
+        m = gt ? w : m;
+      };
+      int r = 0;
+      for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+        VT a0 = q0[0], a1 = q0[n];
+        if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); a1 = sc_(a1, s0, 0); q0[0] = a0; q0[n] = a1; }
+        upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
+        upd2(a1, r + 1, z0, mB[0], cB[0], rB[0]);
+        VT b0 = q1[0], b1 = q1[n];
+        if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); b1 = sc_(b1, s1, 1); q1[0] = b0; q1[n] = b1; }
+        upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
+        upd2(b1, r + 1, z1, mB[1], cB[1], rB[1]);
+      }
+      if (r < n) {
+        VT a0 = q0[0];
+        if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); q0[0] = a0; }
+        upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
+        VT b0 = q1[0];
+        if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); q1[0] = b0; }
+        upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
+      }
+      if constexpr (decltype(do_scale)::value) {
+        *zp0 = sc_(zv0, s0, 0);
+        if (live1) *zp1 = sc_(zv1, s1, 1);
+      } else {
+        *zp0 = zv0;
+        if (live1) *zp1 = zv1;
+      }
+      return;
+    }
+    int r = 0;
+    for (; r + 1 < n; r += 2) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        VT* cell = tile + r * n + col[k];
+        VT v0 = cell[0], v1 = cell[n];
+        if constexpr (decltype(do_scale)::value) {
+          v0 = rescale(v0, k); v1 = rescale(v1, k);
+          cell[0] = v0; cell[n] = v1;
+        }
+        upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
+        upd(v1, r + 1, k, mB[k], cB[k], rB[k]);
+      }
+    }
+    if (r < n) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        VT* cell = tile + r * n + col[k];
+        VT v0 = cell[0];
+        if constexpr (decltype(do_scale)::value) { v0 = rescale(v0, k); cell[0] = v0; }
+        upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
+      }
+    }
+  };
+  if (smode == 0) {
+    stats_rows(std::false_type{});  // lazily scaled layout: u' = lin stays unscaled
+  } else if (smode == 1) {
+    stats_rows(std::true_type{});   // the normalised (norm mode) path
+  } else {
+    const ColOut<VT, CPL> g = stats_generic<VT, CPL>(tile, n, in);
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) { nmax[k] = g.m[k]; ncnt[k] = g.c[k]; nrow[k] = g.r[k]; }
+  }
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    if (!cfree[k]) continue;
+    // merge the odd-row half (ties: counts add, first row = smaller row)
+    if (nmax[k] == NINF || mB[k] > nmax[k]) { nmax[k] = mB[k]; ncnt[k] = cB[k]; nrow[k] = rB[k]; }
+    else if (mB[k] == nmax[k] && mB[k] != NINF) { ncnt[k] += cB[k]; nrow[k] = min(nrow[k], rB[k]); }
+  }
+  ColOut<VT, CPL> o;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) { o.m[k] = nmax[k]; o.c[k] = ncnt[k]; o.r[k] = nrow[k]; }
+  return o;
+}
+
+// Full fp32 velocity pass (the non-incremental case: every entry c1 v, the
+// <= 3 touched rows patched afterwards).  Out of line: in the lazily scaled
+// layout it runs only when a column is renormalised, and keeping it out of
+// the step kernel's body keeps the per-particle path within the
+// instruction cache.  Lazily scaled: v = u * cs, the column factor c1 * cs.
+template <int CPL>
+struct VelIn {
+  int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
+  bool cfree[CPL];
+  float cs[CPL];
+};
+template <int CPL>
+struct VelOut { float total[CPL]; };
+
+template <int G, int CPL>
+__device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn<CPL> in, double c1,
+                                                 double c2r2, double c3r3, double vmax, int v_bounded) {
+  VelOut<CPL> o;
+  int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
+  bool cfree[CPL];
+  float cs[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    col[k] = in.col[k]; zr[k] = in.zr[k]; plr[k] = in.plr[k]; pgr[k] = in.pgr[k];
+    cfree[k] = in.cfree[k]; cs[k] = in.cs[k]; o.total[k] = 0.0f;
+  }
+  // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
+  // x / pl / pg are patched afterwards (sum order is not significant
+  // under the fp32 tolerance).  Lazily scaled layout: v = u * s, the
+  // column factor is c1 * s and the result stays unnormalised (u' = lin).
+  const float c1f = (float)c1;
+  const float vm = (float)vmax;
+  float c1k[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) c1k[k] = c1f * cs[k];
+  float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    tot[k] = 0.f;
+    vx[k] = vl[k] = vg[k] = 0.f;
+    if (cfree[k]) {
+      vx[k] = tile[zr[k] * n + col[k]];
+      vl[k] = tile[plr[k] * n + col[k]];
+      vg[k] = tile[pgr[k] * n + col[k]];
+    }
+  }
+  // two partial sums per column (even / odd rows) break the FADD
+  // dependency chain; the fp32 tolerance admits any summation order
+  float tot2[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) tot2[k] = 0.f;
+  // |c1 v| <= v_max guaranteed for every stored v: the clamp is a no-op
+  const float vmc = v_bounded ? __int_as_float(0x7f800000) : vm;
+  if constexpr (G == 1 && CPL == 2) {
+    // n in 33..64: slot 0 is live in every lane; a dead slot 1 re-runs
+    // slot 0's column with a unit factor (same thread, idempotent),
+    // which keeps the loop branch-free.  Running smem pointers.
+    const bool live1 = cfree[1];
+    float* q0 = reinterpret_cast<float*>(tile) + col[0];
+    float* q1 = reinterpret_cast<float*>(tile) + (live1 ? col[1] : col[0]);
+    const float f0 = c1k[0];
+    const float f1 = live1 ? c1k[1] : 1.0f;
+    const int n2 = 2 * n;
+    auto run = [&](auto clampit) {
+      auto cl = [&](float x) -> float {
+        if constexpr (decltype(clampit)::value) return fminf(fmaxf(x, -vmc), vmc);
+        else return x;
+      };
+      int r = 0;
+      for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+        const float a0 = cl(f0 * q0[0]), a1 = cl(f0 * q0[n]);
+        q0[0] = a0; q0[n] = a1;
+        tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
+        const float b0 = cl(f1 * q1[0]), b1 = cl(f1 * q1[n]);
+        q1[0] = b0; q1[n] = b1;
+        tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
+      }
+      if (r < n) {
+        const float a0 = cl(f0 * q0[0]);
+        q0[0] = a0; tot[0] += fabsf(a0);
+        const float b0 = cl(f1 * q1[0]);
+        q1[0] = b0; tot[1] += fabsf(b0);
+      }
+    };
+    if (v_bounded) run(std::false_type{});
+    else run(std::true_type{});
+  } else {
+    int r = 0;
+    for (; r + 1 < n; r += 2) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+        const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
+        const float l1 = fminf(fmaxf(c1k[k] * cell[n], -vmc), vmc);
+        cell[0] = l0;
+        cell[n] = l1;
+        tot[k] += fabsf(l0);
+        tot2[k] += fabsf(l1);
+      }
+    }
+    if (r < n) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+        const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
+        cell[0] = l0;
+        tot[k] += fabsf(l0);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) tot[k] += tot2[k];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    if (!cfree[k]) continue;
+    const int xr = zr[k], lr = plr[k], gr = pgr[k];
+    float* colp = reinterpret_cast<float*>(tile) + col[k];
+    auto fix = [&](int r, float v0) {
+      const float d2 = (float)((r == lr) - (r == xr));
+      const float d3 = (float)((r == gr) - (r == xr));
+      const float g = fminf(fmaxf(c1k[k] * v0, -vm), vm);
+      // in double: the pulls and the inertia term can cancel
+      const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * ((double)v0 * (double)cs[k])));
+      const float sp = (float)fmin(fmax(l, -vmax), vmax);
+      colp[r * n] = sp;
+      tot[k] += fabsf(sp) - fabsf(g);
+    };
+    fix(xr, vx[k]);
+    if (lr != xr) fix(lr, vl[k]);
+    if (gr != xr && gr != lr) fix(gr, vg[k]);
+    o.total[k] = tot[k];
+  }
+  return o;
+}
+
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 __global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : 1))
@@ -631,7 +919,12 @@ step_kernel(const StepArgs a) {
   const int lane = threadIdx.x & 31;
   unsigned char* gb = smem + (fds ? K::fd_bytes(n) : 0) + (size_t)gidx * K::group_bytes(a.vstride);
   VT* tile = reinterpret_cast<VT*>(gb);   // re-pointed per particle when GT
-  Scratch& sc = *reinterpret_cast<Scratch*>(gb + K::tile_bytes(a.vstride));
+  unsigned char* stg = gb + K::tile_bytes(a.vstride);
+  float* s_col = reinterpret_cast<float*>(stg + K::SCOL);
+  int16_t* s_perm = reinterpret_cast<int16_t*>(stg + K::SPERM);
+  double* s_coef = reinterpret_cast<double*>(stg + K::SCOEF);
+  int64_t* s_cost = reinterpret_cast<int64_t*>(stg + K::SCOST);
+  Scratch& sc = *reinterpret_cast<Scratch*>(stg + K::stage_bytes());
 
   const bool do_vel = a.flags & F_VELOCITY;
   const bool do_agg = a.flags & F_AGGREGATE;
@@ -690,11 +983,38 @@ step_kernel(const StepArgs a) {
   // stopped reading the current one, so the load overlaps the goal and
   // personal-best phases; `loaded` says whether p's load is in flight.
   bool loaded = false;
-  auto issue_load = [&](int64_t pp) {
+  const int vcs = a.vcstride;
+  const uint32_t col_bytes = (uint32_t)(5 * vcs * sizeof(float));
+  // staged perm rows need 4-byte aligned rows (n even)
+  const bool stage_perm = K::STAGE && (n % 2) == 0;
+  const bool stage_cost = K::STAGE && do_cost && a.cost_incremental && !kFloatMat;
+  const bool stage_pl = K::STAGE && do_pbest && do_cost;
+  int cbuf = 0;   // s_cost buffer of the particle being processed
+  auto issue_load = [&](int64_t pp, int buf) {
     if (tid == 0) {
       bulk_wait_read();                 // the previous bulk store has left the tile
-      mbar_arrive_expect_tx(&sc.bar, tile_bytes);
+      mbar_arrive_expect_tx(&sc.bar, tile_bytes + (K::STAGE && lazy ? col_bytes : 0u));
       bulk_load(tile, reinterpret_cast<VT*>(a.V) + pp * a.vstride, tile_bytes, &sc.bar);
+      if (K::STAGE && lazy) bulk_load(s_col, a.vcol + pp * 5 * (int64_t)vcs, col_bytes, &sc.bar);
+    }
+    if constexpr (K::STAGE) {
+      if (stage_perm) {
+        const int nw = n >> 1;
+        const int64_t ss = (int64_t)((unsigned)pp / (unsigned)a.S);
+        for (int w = lane; w < nw; w += 32) {
+          cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
+          if (do_vel) {
+            cp_async4(s_perm + K::NMAX + 2 * w, a.pl_perm + pp * n + 2 * w);
+            cp_async4(s_perm + 2 * K::NMAX + 2 * w, a.pg_perm + ss * n + 2 * w);
+          }
+        }
+      }
+      if (lane == 0) {
+        if (do_vel && a.coef) cp_async16(s_coef, a.coef + 2 * pp);
+        if (stage_cost) cp_async8(s_cost + 2 * buf, reinterpret_cast<const int64_t*>(a.cost) + pp);
+        if (stage_pl) cp_async8(s_cost + 2 * buf + 1, reinterpret_cast<const int64_t*>(a.pl_cost) + pp);
+      }
+      cp_async_commit();
     }
   };
   while (p < a.P) {
@@ -704,9 +1024,16 @@ step_kernel(const StepArgs a) {
     if constexpr (GT) {
       tile = gV;
     } else if (!loaded) {
-      issue_load(p);
+      issue_load(p, cbuf);
     }
     loaded = false;
+    if constexpr (K::STAGE) {
+      // this particle's tile, column state and rows are in shared memory
+      mbar_wait(&sc.bar, phase);
+      phase ^= 1u;
+      cp_async_wait_all();
+      __syncwarp();
+    }
 
     QSB_COUNT(0, 1);
     DrawRow dr;
@@ -727,11 +1054,19 @@ step_kernel(const StepArgs a) {
     for (int k = 0; k < CPL; ++k) {
       col[k] = tid + k * NT;
       cfree[k] = col[k] < n;
-      zr[k] = cfree[k] ? (int)gperm[col[k]] : -1;
       plr[k] = pgr[k] = -1;
-      if (do_vel && cfree[k]) {
-        plr[k] = a.pl_perm[p * n + col[k]];
-        pgr[k] = a.pg_perm[s * n + col[k]];
+      if (stage_perm) {
+        zr[k] = cfree[k] ? (int)s_perm[col[k]] : -1;
+        if (do_vel && cfree[k]) {
+          plr[k] = s_perm[K::NMAX + col[k]];
+          pgr[k] = s_perm[2 * K::NMAX + col[k]];
+        }
+      } else {
+        zr[k] = cfree[k] ? (int)gperm[col[k]] : -1;
+        if (do_vel && cfree[k]) {
+          plr[k] = a.pl_perm[p * n + col[k]];
+          pgr[k] = a.pg_perm[s * n + col[k]];
+        }
       }
     }
     // lazily scaled layout: column scale s, sum A of |u| over the column,
@@ -740,23 +1075,25 @@ step_kernel(const StepArgs a) {
     float cs[CPL], cM[CPL];
     double cA[CPL];
     int cCR[CPL];
-    const int vcs = a.vcstride;
     float* vcp = lazy ? a.vcol + p * 5 * (int64_t)vcs : nullptr;
+    const float* vcr = K::STAGE ? s_col : vcp;   // staged copy when one-warp
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       cs[k] = 1.0f; cA[k] = 0.0; cM[k] = 0.0f; cCR[k] = 0;
       if (lazy && cfree[k]) {
-        cs[k] = vcp[col[k]];
-        cA[k] = __hiloint2double(__float_as_int(vcp[2 * vcs + col[k]]),
-                                 __float_as_int(vcp[vcs + col[k]]));
-        cM[k] = vcp[3 * vcs + col[k]];
-        cCR[k] = __float_as_int(vcp[4 * vcs + col[k]]);
+        cs[k] = vcr[col[k]];
+        cA[k] = __hiloint2double(__float_as_int(vcr[2 * vcs + col[k]]),
+                                 __float_as_int(vcr[vcs + col[k]]));
+        cM[k] = vcr[3 * vcs + col[k]];
+        cCR[k] = __float_as_int(vcr[4 * vcs + col[k]]);
       }
     }
     double c2r2 = 0.0, c3r3 = 0.0;
     if (do_vel) {
-      if (a.coef) { c2r2 = a.coef[2 * p]; c3r3 = a.coef[2 * p + 1]; }
-      else {
+      if (a.coef) {
+        const double* cf = K::STAGE ? s_coef : a.coef + 2 * p;
+        c2r2 = cf[0]; c3r3 = cf[1];
+      } else {
         c2r2 = __dmul_rn(a.c2, dr.at(0));   // engine.py:198-199: c2 * r2, c3 * r3
         c3r3 = __dmul_rn(a.c3, dr.at(1));
       }
@@ -782,7 +1119,7 @@ step_kernel(const StepArgs a) {
       if (!incr) QSB_COUNT(8, 1);
     }
 
-    if constexpr (!GT) {
+    if constexpr (!GT && !K::STAGE) {
       mbar_wait(&sc.bar, phase);
       phase ^= 1u;
     }
@@ -885,114 +1222,16 @@ step_kernel(const StepArgs a) {
         }
         fence_proxy_async_smem();   // generic tile writes before the next bulk load
       } else {
-        // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
-        // x / pl / pg are patched afterwards (sum order is not significant
-        // under the fp32 tolerance).  Lazily scaled layout: v = u * s, the
-        // column factor is c1 * s and the result stays unnormalised (u' = lin).
-        const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
-        const float vm = (float)a.vmax;
-        float c1k[CPL];
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) c1k[k] = c1f * cs[k];
-        float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
+        VelIn<CPL> vi;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          tot[k] = 0.f;
-          vx[k] = vl[k] = vg[k] = 0.f;
-          if (cfree[k]) {
-            vx[k] = tile[zr[k] * n + col[k]];
-            vl[k] = tile[plr[k] * n + col[k]];
-            vg[k] = tile[pgr[k] * n + col[k]];
-          }
+          vi.col[k] = col[k]; vi.zr[k] = zr[k]; vi.plr[k] = plr[k]; vi.pgr[k] = pgr[k];
+          vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k];
         }
-        // two partial sums per column (even / odd rows) break the FADD
-        // dependency chain; the fp32 tolerance admits any summation order
-        float tot2[CPL];
+        const VelOut<CPL> vo = vel_full_f32<G, CPL>(reinterpret_cast<float*>(tile), n, vi, a.c1, c2r2,
+                                                    c3r3, a.vmax, a.v_bounded);
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) tot2[k] = 0.f;
-        // |c1 v| <= v_max guaranteed for every stored v: the clamp is a no-op
-        const float vmc = a.v_bounded ? __int_as_float(0x7f800000) : vm;
-        if constexpr (G == 1 && CPL == 2) {
-          // n in 33..64: slot 0 is live in every lane; a dead slot 1 re-runs
-          // slot 0's column with a unit factor (same thread, idempotent),
-          // which keeps the loop branch-free.  Running smem pointers.
-          const bool live1 = cfree[1];
-          float* q0 = reinterpret_cast<float*>(tile) + col[0];
-          float* q1 = reinterpret_cast<float*>(tile) + (live1 ? col[1] : col[0]);
-          const float f0 = c1k[0];
-          const float f1 = live1 ? c1k[1] : 1.0f;
-          const int n2 = 2 * n;
-          auto run = [&](auto clampit) {
-            auto cl = [&](float x) -> float {
-              if constexpr (decltype(clampit)::value) return fminf(fmaxf(x, -vmc), vmc);
-              else return x;
-            };
-            int r = 0;
-            for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
-              const float a0 = cl(f0 * q0[0]), a1 = cl(f0 * q0[n]);
-              q0[0] = a0; q0[n] = a1;
-              tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
-              const float b0 = cl(f1 * q1[0]), b1 = cl(f1 * q1[n]);
-              q1[0] = b0; q1[n] = b1;
-              tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
-            }
-            if (r < n) {
-              const float a0 = cl(f0 * q0[0]);
-              q0[0] = a0; tot[0] += fabsf(a0);
-              const float b0 = cl(f1 * q1[0]);
-              q1[0] = b0; tot[1] += fabsf(b0);
-            }
-          };
-          if (a.v_bounded) run(std::false_type{});
-          else run(std::true_type{});
-        } else {
-          int r = 0;
-          for (; r + 1 < n; r += 2) {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              if (!cfree[k]) continue;
-              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
-              const float l1 = fminf(fmaxf(c1k[k] * cell[n], -vmc), vmc);
-              cell[0] = l0;
-              cell[n] = l1;
-              tot[k] += fabsf(l0);
-              tot2[k] += fabsf(l1);
-            }
-          }
-          if (r < n) {
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-              if (!cfree[k]) continue;
-              float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-              const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
-              cell[0] = l0;
-              tot[k] += fabsf(l0);
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) tot[k] += tot2[k];
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          if (!cfree[k]) continue;
-          const int xr = zr[k], lr = plr[k], gr = pgr[k];
-          float* colp = reinterpret_cast<float*>(tile) + col[k];
-          auto fix = [&](int r, float v0) {
-            const float d2 = (float)((r == lr) - (r == xr));
-            const float d3 = (float)((r == gr) - (r == xr));
-            const float g = fminf(fmaxf(c1k[k] * v0, -vm), vm);
-            // in double: the pulls and the inertia term can cancel
-            const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, a.c1 * ((double)v0 * (double)cs[k])));
-            const float sp = (float)fmin(fmax(l, -a.vmax), a.vmax);
-            colp[r * n] = sp;
-            tot[k] += fabsf(sp) - fabsf(g);
-          };
-          fix(xr, vx[k]);
-          if (lr != xr) fix(lr, vl[k]);
-          if (gr != xr && gr != lr) fix(gr, vg[k]);
-          total[k] = (VT)tot[k];
-        }
+        for (int k = 0; k < CPL; ++k) total[k] = (VT)vo.total[k];
       }
     }
 
@@ -1084,129 +1323,18 @@ step_kernel(const StepArgs a) {
     }
     if (stats_done) {
     } else if (do_agg) {
-      // Max / tie count / first row over the non-z rows (the z row is masked
-      // to -inf; stored values are finite), accumulated separately over even
-      // and odd rows (two independent dependency chains) and merged.  A
-      // half holding only the z row keeps max = -inf and is ignored.
-      const VT NINF = (VT)(-INFINITY);
-      VT mB[CPL];
-      int cB[CPL], rB[CPL];
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) { mB[k] = NINF; cB[k] = 0; rB[k] = -1; }
-      auto upd = [&](VT v, int r, int k, VT& m, int& c, int& rr) {
-        const VT w = r == zr[k] ? NINF : v;
-        const bool gt = w > m;
-        c = gt ? 1 : c + (w == m ? 1 : 0);
-        rr = gt ? r : rr;
-        m = gt ? w : m;
-      };
-      auto stats_rows = [&](auto do_scale) {
-        if constexpr (G == 1 && CPL == 2) {
-          // branch-free form (see the velocity loop): a dead slot 1 rescans
-          // slot 0's column with a unit factor; its statistics are unused
-          const bool live1 = cfree[1];
-          VT* q0 = tile + col[0];
-          VT* q1 = tile + (live1 ? col[1] : col[0]);
-          const VT s0 = inv[0], s1 = live1 ? inv[1] : (VT)1;
-          // the z cells are parked at -inf during the scan (restored below),
-          // so the loop needs no per-row z test
-          VT* zp0 = q0 + zr[0] * n;
-          VT* zp1 = q1 + (live1 ? zr[1] : zr[0]) * n;
-          const VT zv0 = *zp0;
-          const VT zv1 = live1 ? *zp1 : (VT)0;
-          *zp0 = NINF;
-          if (live1) *zp1 = NINF;
-          const int z0 = -1, z1 = -1;
-          const int n2 = 2 * n;
-          auto sc_ = [&](VT v, VT f, int k) -> VT {
-            if constexpr (sizeof(VT) == 8) return k == 0 || live1 ? __ddiv_rn(v, total[k]) : v;
-            else return v * f;
-          };
-          auto upd2 = [&](VT w, int r, int, VT& m, int& c, int& rr) {
-            const bool gt = w > m;
-            c = gt ? 1 : c + (w == m ? 1 : 0);
-            rr = gt ? r : rr;
-            m = gt ? w : m;
-          };
-          int r = 0;
-          for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
-            VT a0 = q0[0], a1 = q0[n];
-            if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); a1 = sc_(a1, s0, 0); q0[0] = a0; q0[n] = a1; }
-            upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
-            upd2(a1, r + 1, z0, mB[0], cB[0], rB[0]);
-            VT b0 = q1[0], b1 = q1[n];
-            if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); b1 = sc_(b1, s1, 1); q1[0] = b0; q1[n] = b1; }
-            upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
-            upd2(b1, r + 1, z1, mB[1], cB[1], rB[1]);
-          }
-          if (r < n) {
-            VT a0 = q0[0];
-            if constexpr (decltype(do_scale)::value) { a0 = sc_(a0, s0, 0); q0[0] = a0; }
-            upd2(a0, r, z0, nmax[0], ncnt[0], nrow[0]);
-            VT b0 = q1[0];
-            if constexpr (decltype(do_scale)::value) { b0 = sc_(b0, s1, 1); q1[0] = b0; }
-            upd2(b0, r, z1, nmax[1], ncnt[1], nrow[1]);
-          }
-          if constexpr (decltype(do_scale)::value) {
-            *zp0 = sc_(zv0, s0, 0);
-            if (live1) *zp1 = sc_(zv1, s1, 1);
-          } else {
-            *zp0 = zv0;
-            if (live1) *zp1 = zv1;
-          }
-          return;
-        }
-        int r = 0;
-        for (; r + 1 < n; r += 2) {
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            if (!cfree[k]) continue;
-            VT* cell = tile + r * n + col[k];
-            VT v0 = cell[0], v1 = cell[n];
-            if constexpr (decltype(do_scale)::value) {
-              v0 = rescale(v0, k); v1 = rescale(v1, k);
-              cell[0] = v0; cell[n] = v1;
-            }
-            upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
-            upd(v1, r + 1, k, mB[k], cB[k], rB[k]);
-          }
-        }
-        if (r < n) {
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            if (!cfree[k]) continue;
-            VT* cell = tile + r * n + col[k];
-            VT v0 = cell[0];
-            if constexpr (decltype(do_scale)::value) { v0 = rescale(v0, k); cell[0] = v0; }
-            upd(v0, r, k, nmax[k], ncnt[k], nrow[k]);
-          }
-        }
-      };
+      ColIn<VT, CPL> in;
       bool all_scale = true;
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) all_scale &= scale[k] || !cfree[k];
-      if (kLazy && lazy) {
-        stats_rows(std::false_type{});  // lazily scaled layout: u' = lin stays unscaled
-      } else if (__all_sync(FULL, all_scale)) {
-        stats_rows(std::true_type{});   // the normalised (norm mode) hot path
-      } else {
-        ColIn<VT, CPL> in;
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          in.col[k] = col[k]; in.zr[k] = zr[k]; in.cfree[k] = cfree[k]; in.scale[k] = scale[k];
-          in.total[k] = total[k]; in.inv[k] = inv[k];
-        }
-        const ColOut<VT, CPL> o = stats_generic<VT, CPL>(tile, n, in);
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) { nmax[k] = o.m[k]; ncnt[k] = o.c[k]; nrow[k] = o.r[k]; }
-      }
-#pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        if (!cfree[k]) continue;
-        // merge the odd-row half (ties: counts add, first row = smaller row)
-        if (nmax[k] == NINF || mB[k] > nmax[k]) { nmax[k] = mB[k]; ncnt[k] = cB[k]; nrow[k] = rB[k]; }
-        else if (mB[k] == nmax[k] && mB[k] != NINF) { ncnt[k] += cB[k]; nrow[k] = min(nrow[k], rB[k]); }
+        in.col[k] = col[k]; in.zr[k] = zr[k]; in.cfree[k] = cfree[k]; in.scale[k] = scale[k];
+        in.total[k] = total[k]; in.inv[k] = inv[k];
+        all_scale &= scale[k] || !cfree[k];
       }
+      const int smode = (kLazy && lazy) ? 0 : (__all_sync(FULL, all_scale) ? 1 : 2);
+      const ColOut<VT, CPL> so = stats_pass<VT, G, CPL>(tile, n, in, smode);
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) { nmax[k] = so.m[k]; ncnt[k] = so.c[k]; nrow[k] = so.r[k]; }
     } else if (!lazy) {
 #pragma unroll 1
       for (int r = 0; r < n; ++r) {
@@ -1669,7 +1797,7 @@ step_kernel(const StepArgs a) {
       if constexpr (!GT) {
         // the tile is no longer read for this particle: prefetch the next one
         p_next = a.work ? bcast(q_next) : p + ngroups;
-        if (p_next < a.P) { issue_load(p_next); loaded = true; }
+        if (p_next < a.P) { issue_load(p_next, cbuf ^ 1); loaded = true; }
       }
       int16_t* gnew = a.perm_new + p * n;
       #pragma unroll 1
@@ -1678,6 +1806,7 @@ step_kernel(const StepArgs a) {
 
     // ================= phase 3: goal  sum_ij F[i,j] * D[perm_i, perm_j]
     bool cost_done = false;
+    int64_t ncost = 0;   // the new goal (raw bits for doubles), valid on tid 0 when cost_done
     if constexpr (G == 1 && !kFloatMat) {
       // Incremental goal (integral instances, one-warp groups): most columns
       // keep their row (the bulk step re-selects the z cells), so with C the
@@ -1725,7 +1854,9 @@ step_kernel(const StepArgs a) {
           const int64_t delta = warp_sum_i64((int64_t)acc);
           if (tid == 0) {
             int64_t* cp = reinterpret_cast<int64_t*>(a.cost);
-            cp[p] = (int64_t)((uint64_t)cp[p] + (uint64_t)delta);
+            const int64_t old = stage_cost ? s_cost[2 * cbuf] : cp[p];
+            ncost = (int64_t)((uint64_t)old + (uint64_t)delta);
+            cp[p] = ncost;
           }
           cost_done = true;
         }
@@ -1734,6 +1865,8 @@ step_kernel(const StepArgs a) {
     if (do_cost && !cost_done) {
       const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane, a.acc32);
       if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
+      ncost = tot;
+      cost_done = true;
     }
 
     // ================= phase 4a: personal best (engine.py:211-215)
@@ -1741,16 +1874,16 @@ step_kernel(const StepArgs a) {
       Sync::sync();
       if (tid == 0) {
         bool imp;
+        // the new goal from this step (register) and the staged pl_cost
+        const int64_t cvb = cost_done ? ncost : reinterpret_cast<int64_t*>(a.cost)[p];
+        const int64_t plb = stage_pl ? s_cost[2 * cbuf + 1] : reinterpret_cast<int64_t*>(a.pl_cost)[p];
         if constexpr (kFloatMat) {
-          const double cv = reinterpret_cast<double*>(a.cost)[p];
-          double* pl = reinterpret_cast<double*>(a.pl_cost);
-          imp = cv < pl[p];
-          if (imp) pl[p] = cv;
+          const double cv = __longlong_as_double(cvb);
+          imp = cv < __longlong_as_double(plb);
+          if (imp) reinterpret_cast<double*>(a.pl_cost)[p] = cv;
         } else {
-          const int64_t cv = reinterpret_cast<int64_t*>(a.cost)[p];
-          int64_t* pl = reinterpret_cast<int64_t*>(a.pl_cost);
-          imp = cv < pl[p];
-          if (imp) pl[p] = cv;
+          imp = cvb < plb;
+          if (imp) reinterpret_cast<int64_t*>(a.pl_cost)[p] = cvb;
         }
         a.improved[p] = imp ? 1 : 0;
         sc.ssel[2] = imp;
@@ -1765,6 +1898,7 @@ step_kernel(const StepArgs a) {
     Sync::sync();
     if (p_next < 0) p_next = a.work ? bcast(q_next) : p + ngroups;
     p = p_next;
+    cbuf ^= 1;
   }
   if (!GT && tid == 0) bulk_wait_all();
 }
