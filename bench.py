@@ -99,12 +99,21 @@ def workload(args, n_gpus):
                   f"{args.swarms * args.swarm_size * args.n * args.n * (4 if args.precision == 'fp32' else 8) / 1e6:.0f} MB > 126 MB)"}
 
 
-def bytes_per_particle(n, S, sv):
-    """Algorithmic HBM bytes of the fused step per particle-iteration:
-    V read + write (2 n^2 sV), perm / pl_perm read + perm_new write (6n),
-    swarm best read amortised (2n/S), cost write, pl_cost read, improved
-    flag (17)."""
-    return 2 * n * n * sv + 6 * n + 2 * n / S + 17
+def bytes_per_particle(n, S, sv, lazy=False, incremental_cost=True):
+    """Algorithmic HBM bytes of one fused step per particle-iteration.
+
+    Stored-v layout (fp64, or fp32 without the lazy column scale): V read +
+    write (2 n^2 sV).  Lazily scaled fp32 layout: the tile is
+    read (4 n^2), only the <= 3n entries x / pl / pg touch are written (12n),
+    and the column state is read and written (2 * 20 * ceil4(n)).  Both:
+    perm / pl_perm read + perm_new write (6n), swarm best row amortised
+    (2n/S), (c2 r2, c3 r3) written by the draw pre-pass and read (32), cost
+    read (incremental goal) and written, pl_cost read, improved flag (25)."""
+    common = 6 * n + 2 * n / S + 32 + (25 if incremental_cost else 17)
+    if lazy:
+        vcs = (n + 3) // 4 * 4
+        return 4 * n * n + 12 * n + 40 * vcs + common
+    return 2 * n * n * sv + common
 
 
 # ------------------------------------------------------------- clocks
@@ -184,14 +193,14 @@ class KernelTimer:
         return sum(d) / len(d) if d else None
 
 
-def traffic_from_profile(n, precision, particles):
+def traffic_from_profile(n, precision, particles, prefix=""):
     """ncu DRAM bytes per launch of the fused kernel, from profiles/ (or None)."""
     p = ROOT / "profiles" / "ncu_step_summary.json"
     if not p.exists():
         return None
     try:
         rec = json.loads(p.read_text())
-        key = f"n{n}_{precision}_P{particles}"
+        key = f"{prefix}n{n}_{precision}_P{particles}"
         return rec.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
@@ -288,6 +297,7 @@ def main():
     if args.velocity_only:
         from paper_1504_05158_b200 import _lib
         flags = _lib.PHASE_VELOCITY | _lib.PHASE_STORE_V
+        state.set_lazy_scale(False)   # the streaming velocity pass over the stored-v layout
 
     def one_step():
         if flags is None:
@@ -395,9 +405,10 @@ def main():
 
     # ---- roofline of the fused kernel
     sv = 4 if cfg.precision == "fp32" else 8
-    B = bytes_per_particle(args.n, args.swarm_size, sv)
+    lazy = getattr(state, "d_vcol", None) is not None
+    B = bytes_per_particle(args.n, args.swarm_size, sv, lazy=lazy)
     if flags is not None:
-        B = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size
+        B = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
     per_launch = B * state.local_particles
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
@@ -407,8 +418,9 @@ def main():
     achieved = per_launch / (kern_max / 1000.0) / 1e9 if kern_max else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": traffic_from_profile(args.n, cfg.precision, state.local_particles),
-                "kernel": "step_kernel (fused velocity+aggregation+goal+pbest)" if flags is None
+                "traffic": traffic_from_profile(args.n, cfg.precision, state.local_particles,
+                                                "velocity_only_" if flags is not None else ""),
+                "kernel": "coef_kernel + step_kernel (draw pre-pass; fused velocity+aggregation+goal+pbest)" if flags is None
                           else "step_kernel velocity-only build",
                 "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"}
