@@ -990,6 +990,13 @@ step_kernel(const StepArgs a) {
   const bool stage_cost = K::STAGE && do_cost && a.cost_incremental && !kFloatMat;
   const bool stage_pl = K::STAGE && do_pbest && do_cost;
   int cbuf = 0;   // s_cost buffer of the particle being processed
+  // p / S via a reciprocal: p < 2^24 (host limit), so p * (1/S) is within
+  // 2^-28 of p / S, while a non-zero fractional part of p / S is at least
+  // 1 / S >= 2^-24: the 2^-26 nudge makes the truncation exact
+  const double inv_s = 1.0 / (double)a.S;
+  auto swarm_of = [&](int64_t pp) -> int64_t {
+    return (int64_t)__fma_rn((double)pp, inv_s, 0x1p-26);
+  };
   auto issue_load = [&](int64_t pp, int buf) {
     if (tid == 0) {
       bulk_wait_read();                 // the previous bulk store has left the tile
@@ -1000,7 +1007,7 @@ step_kernel(const StepArgs a) {
     if constexpr (K::STAGE) {
       if (stage_perm) {
         const int nw = n >> 1;
-        const int64_t ss = (int64_t)((unsigned)pp / (unsigned)a.S);
+        const int64_t ss = swarm_of(pp);
         for (int w = lane; w < nw; w += 32) {
           cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
           if (do_vel) {
@@ -1049,7 +1056,7 @@ step_kernel(const StepArgs a) {
     int zr[CPL], col[CPL], plr[CPL], pgr[CPL];
     bool cfree[CPL];
     const int16_t* gperm = a.perm + p * n;
-    const int64_t s = (int64_t)((unsigned)p / (unsigned)a.S);   // P < 2^31 (host-checked)
+    const int64_t s = swarm_of(p);
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       col[k] = tid + k * NT;
@@ -1170,12 +1177,11 @@ step_kernel(const StepArgs a) {
         // touched entries get u' = lin / (c1 s).  Since total = c1 s A' with
         // A' = sum |u'|, s' = 1 / A'.  The all-rows statistics are updated
         // entry by entry (an entry leaving the maximum forces a rescan).
-        const float c1f = (float)a.c1, c2f = (float)c2r2, c3f = (float)c3r3;
         const float vm = (float)a.vmax;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           if (!cfree[k]) continue;
-          const int xr = zr[k], lr = plr[k], gr = pgr[k], c = col[k];
+          const int xr = zr[k], lr = plr[k], gr = pgr[k];
           // lin of a touched entry is formed in double (the pulls and the
           // inertia term can cancel), then rounded once; u' = lin / (c1 s)
           const double c1sd = a.c1 * (double)cs[k];
@@ -1186,25 +1192,28 @@ step_kernel(const StepArgs a) {
           const int zp = cCR[k] & 0xff;
           double Ad = cA[k];
           bool bad = false;
-          float* colp = reinterpret_cast<float*>(tile) + c;
-          auto upd = [&](int r) {
-            const int i2 = (r == lr) - (r == xr), i3 = (r == gr) - (r == xr);
-            if (i2 == 0 && i3 == 0) return;
+          float* colp = reinterpret_cast<float*>(tile) + col[k];
+          float* gcol = reinterpret_cast<float*>(gV) + col[k];
+          // the touched rows and their pulls c2 r2 (pl - x) + c3 r3 (pg - x):
+          //   x row: -c2 r2 [x != pl] - c3 r3 [x != pg] (none: unchanged)
+          //   pl row (!= x): c2 r2 + c3 r3 [pl == pg];  pg row (!= x, pl): c3 r3
+          const double offx = -(xr != lr ? c2r2 : 0.0) - (xr != gr ? c3r3 : 0.0);
+          const double offl = c2r2 + (lr == gr ? c3r3 : 0.0);
+          auto upd = [&](int r, double off) {
             const float u = colp[r * n];
-            const float lin = fminf(fmaxf((float)fma(c3r3, (double)i3, fma(c2r2, (double)i2, c1sd * (double)u)),
-                                          -vm), vm);
+            const float lin = fminf(fmaxf((float)fma(c1sd, (double)u, off), -vm), vm);
             const float u2 = lin * rc;
             colp[r * n] = u2;
-            if (store_v) reinterpret_cast<float*>(gV)[r * n + c] = u2;
+            if (store_v) gcol[r * n] = u2;
             Ad += (double)fabsf(u2) - (double)fabsf(u);
             if (r == zp) return;
             if (u2 > M) { M = u2; cnt = 1; R = r; }
             else if (u == M) { if (u2 < M && (--cnt == 0 || R == r)) bad = true; }
             else if (u2 == M) { ++cnt; R = min(R, r); }
           };
-          upd(xr);
-          if (lr != xr) upd(lr);
-          if (gr != xr && gr != lr) upd(gr);
+          if (offx != 0.0) upd(xr, offx);
+          if (lr != xr) upd(lr, offl);
+          if (gr != xr && gr != lr) upd(gr, c3r3);
           if (xr != zp) {
             // the excluded row moves from zp to this step's z row xr
             const float uo = colp[zp * n];
@@ -1246,7 +1255,7 @@ step_kernel(const StepArgs a) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       nmax[k] = (VT)(-INFINITY); ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
-      scale[k] = cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
+      scale[k] = !lazy && cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
       inv[k] = (VT)1;
       if constexpr (sizeof(VT) == 4) inv[k] = scale[k] ? 1.0f / total[k] : 1.0f;
     }
@@ -1317,7 +1326,7 @@ step_kernel(const StepArgs a) {
         // column: no normalisation
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-          sK[k] = (a.normalize && cA[k] > 0.0) ? 1.0f / (float)cA[k] : (incr ? total[k] : 1.0f);
+          sK[k] = (a.normalize && cA[k] > 0.0) ? __frcp_rn((float)cA[k]) : (incr ? total[k] : 1.0f);
         stats_done = true;
       }
     }
@@ -1436,16 +1445,26 @@ step_kernel(const StepArgs a) {
             // the tie ballot (_batch.py:155-170).
             const int kf = n - rnd;
             if (!restricted && kf <= 5) {
+              // ascending lists of the free rows (sc.srow) and columns
+              // (sc.sorder), each entry written by its owner lane
+              const unsigned lt = (1u << lane) - 1u;
+              const unsigned rl = (unsigned)rf.w[0], rh = (unsigned)(rf.w[0] >> 32);
+              if ((rl >> lane) & 1u) sc.srow[__popc(rl & lt)] = (uint16_t)lane;
+              if ((rh >> lane) & 1u) sc.srow[__popc(rl) + __popc(rh & lt)] = (uint16_t)(lane + 32);
               const unsigned cb0 = __ballot_sync(FULL, cfree[0]);
-              const unsigned cb1 = CPL == 2 ? __ballot_sync(FULL, cfree[CPL - 1]) : 0u;
-              const int ei = lane / kf, ej = lane - (lane / kf) * kf;
+              if (cfree[0]) sc.sorder[__popc(cb0 & lt)] = (uint8_t)col[0];
+              if constexpr (CPL == 2) {
+                const unsigned cb1 = __ballot_sync(FULL, cfree[1]);
+                if (cfree[1]) sc.sorder[__popc(cb0) + __popc(cb1 & lt)] = (uint8_t)col[1];
+              }
+              __syncwarp();
+              const int ei = lane / kf, ej = lane - ei * kf;
               bool act = lane < kf * kf;
               int er = 0, ec = 0;
               uint64_t ekey = 0;
               if (act) {
-                const unsigned rl = (unsigned)rf.w[0], rh = (unsigned)(rf.w[0] >> 32);
-                er = ei < __popc(rl) ? nth_set_bit32(rl, ei) : 32 + nth_set_bit32(rh, ei - __popc(rl));
-                ec = ej < __popc(cb0) ? nth_set_bit32(cb0, ej) : 32 + nth_set_bit32(cb1, ej - __popc(cb0));
+                er = sc.srow[ei];
+                ec = sc.sorder[ej];
                 ekey = mkey(tile, sc.sS, n, er, ec, (int)sc.szr[ec]);
               }
 #pragma unroll 1
@@ -1468,8 +1487,8 @@ step_kernel(const StepArgs a) {
                   QSB_COUNT(4, 1);
                 }
                 if (lane == src) sc.sperm[ec] = (uint8_t)er;
-                const int si = src / kf;
-                act = act && ei != si && ej != src - si * kf;
+                const int si = __shfl_sync(FULL, ei, src), sj = __shfl_sync(FULL, ej, src);
+                act = act && ei != si && ej != sj;
               }
               __syncwarp();
               break;
