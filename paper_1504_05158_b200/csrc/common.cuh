@@ -41,7 +41,19 @@ __device__ __forceinline__ PhiloxBlock philox4x64_10(uint64_t c0, uint64_t k0, u
 // few times per particle, and inlining 10 rounds at every call site bloats
 // the step kernel beyond the instruction cache.
 __device__ __noinline__ PhiloxBlock philox_block_call(uint64_t c0, uint64_t k0, uint64_t k1) {
-  return philox4x64_10(c0, k0, k1);
+  // rounds kept rolled: this copy serves tie draws inside the step kernel,
+  // where a small code footprint matters more than the loop overhead
+  uint64_t c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll 1
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B97F4A7C15ULL; k1 += 0xBB67AE8584CAA73BULL; }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+    const uint64_t lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  PhiloxBlock b; b.v[0] = c0; b.v[1] = c1; b.v[2] = c2; b.v[3] = c3;
+  return b;
 }
 
 __device__ __forceinline__ double u64_to_unit(uint64_t u) {
