@@ -1115,12 +1115,15 @@ step_kernel(const StepArgs a) {
     if (lazy && do_vel) {
       bool ok = a.v_bounded && a.c1 > 0.0;
       const float c1f = (float)a.c1;
+      // |lin| of a touched entry is at most lb (the clamp, and c1 + c2 + c3
+      // for normalised columns), so u' = lin / (c1 s) stays below 2^125
+      const float lb = fminf((float)a.vmax, a.normalize ? (float)(a.c1 + a.c2 + a.c3) : INFINITY);
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
         const float c1s = c1f * cs[k];
-        ok &= cM[k] == cM[k] && cs[k] >= 0x1p-60f && cs[k] <= 0x1p60f && c1s >= 0x1p-100f &&
-              c1s <= 0x1p100f;
+        ok &= cM[k] == cM[k] && cs[k] >= 0x1p-110f && cs[k] <= 0x1p110f && c1s >= 0x1p-120f &&
+              c1s <= 0x1p120f && c1s >= lb * 0x1p-125f;
       }
       incr = __all_sync(FULL, ok);
       if (!incr) QSB_COUNT(8, 1);

@@ -15,7 +15,7 @@ cfg = qsb.SolverConfig(swarms=80, swarm_size=100, seed=1, precision=prec, init="
 st = qsb.init_population(cfg, inst)
 buf = (ctypes.c_ulonglong * 12)()
 names = ["particles", "normal_rounds", "bulk_steps", "bulk_cells", "tie_rounds", "warp_tie", "slow_tie",
-         "rescans", "full_pass", "incr_rescans", "incr_unknown"]
+         "rescans", "full_pass", "incr_rescans", "incr_unknown", "renorm"]
 L.qsb_debug_counters(buf)
 for t in range(1, 401):
     qsb.step(st, inst, cfg)
@@ -23,7 +23,7 @@ for t in range(1, 401):
         torch.cuda.synchronize()
         L.qsb_debug_counters(buf)
         P = buf[0]
-        print(t, {names[i]: round(buf[i] / P, 3) for i in range(1, 11)})
+        print(t, {names[i]: round(buf[i] / P, 3) for i in range(1, 12)})
     else:
         torch.cuda.synchronize()
         L.qsb_debug_counters(buf)
