@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 300 -c 1 -o gpurun_out/prof_late python scripts/diag_steps.py fp32 302 > gpurun_out/ncu_late.log 2>&1
+tail -1 gpurun_out/ncu_late.log
