@@ -232,6 +232,111 @@ def test_fp32_velocity_column_scaled_tolerance(name, warm, lazy, golden_instance
     del v_before
 
 
+def _lazy_state_checks(st, n, normalised=True):
+    """The lazily scaled layout's column state matches the stored tile."""
+    import torch
+    p = st.local_particles
+    u = st.d_V[:, :n * n].view(p, n, n).double().cpu().numpy()
+    vc = st.d_vcol.cpu()
+    s = vc[:, 0, :n].double().numpy()
+    words = vc.view(torch.int32).numpy().astype(np.int64) & 0xFFFFFFFF
+    A = ((words[:, 2, :n] << 32) | words[:, 1, :n]).view(np.float64)
+    M = vc[:, 3, :n].double().numpy()
+    cr = vc[:, 4, :n].view(torch.int32).numpy()
+    assert np.isfinite(s).all() and (s > 0).all()
+    known = ~np.isnan(M)
+    zp = cr & 0xFF
+    rows = np.arange(n)[None, :, None]
+    w = np.where(rows == zp[:, None, :], -np.inf, u)
+    mx = w.max(axis=1)
+    assert np.array_equal(M[known], mx[known])
+    assert np.array_equal((cr >> 16)[known], (w == mx[:, None, :]).sum(axis=1)[known])
+    assert np.array_equal(((cr >> 8) & 0xFF)[known], (w == mx[:, None, :]).argmax(axis=1)[known])
+    tot = np.abs(u).sum(axis=1)
+    rel = np.abs(A - tot) / np.where(tot > 0, tot, 1.0)
+    assert rel[known].max() <= 1e-6, rel[known].max()
+    if normalised:
+        colsum = np.abs(st.V).sum(axis=1)
+        assert np.allclose(colsum[colsum > 0], 1.0, rtol=2e-5, atol=0)
+    return known
+
+
+@pytest.mark.parametrize("n", [7, 33, 50, 60, 64])
+@pytest.mark.parametrize("coef", [
+    dict(c1=0.8, c2=0.5, c3=0.5),                                   # norm, second-target
+    dict(c1=0.7, c2=1.0, c3=1.0, v_max=0.3),                        # the clamp bites
+    dict(c1=0.9, c2=0.5, c3=0.5, sv_mode="raw"),                    # raw: no normalisation
+    dict(c1=0.0, c2=0.5, c3=0.5),                                   # c1 = 0: full pass each step
+    dict(c1=0.8, c2=0.5, c3=0.5, sx_mode="global-max"),
+    dict(c1=0.8, c2=0.5, c3=0.5, sx_mode="pick-column"),
+])
+def test_fp32_lazy_layout_matrix(n, coef):
+    """fp32 (lazily scaled for n <= 64): after warm steps, one step replayed
+    on the f64 oracle from the GPU's own state matches within the
+    column-scaled 1e-5 rule, aggregation and goal exactly; the column state
+    stays consistent with the tile."""
+    inst = qsb.taillard_uniform(n)
+    cf = qsb.PsoCoefficients(**coef)
+    cfg = qsb.SolverConfig(swarms=6, swarm_size=20, seed=n, precision="fp32", coefficients=cf,
+                           migration_factor=0.3)
+    st = qsb.init_population(cfg, inst)
+    for _ in range(9):
+        qsb.step(st, inst, cfg)
+    if st.d_vcol is not None:
+        _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
+    ost = orc.init_population(6, 20, n, inst.flow, inst.distance, seed=n)
+    ost.X, ost.perms = st.X, st.perms
+    ost.PL, ost.pl_perms, ost.pl_cost = st.PL, st.pl_perms, st.pl_cost
+    b = st.bests
+    ost.pg_mats, ost.pg_perms, ost.pg_costs = b.matrices, b.perms, b.costs
+    ost.V = st.V.astype(np.float64)
+    ost.t = st.t
+    qsb.step(st, inst, cfg)
+    orc.step(ost, inst.flow, inst.distance, **orc.coeff_kwargs(cfg))
+    got = st.V.astype(np.float64)
+    ref = ost.V
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    err = np.abs(got - ref) / np.where(scale > 0, scale, 1.0)
+    assert err.max() <= 1e-5, err.max()
+    x = orc.matrices_from_perms(np.asarray(ost.perms_new), n)
+    draws = orc.step_draws(cfg.seed, st.t, cfg.num_particles, n)
+    out_mat = np.zeros_like(x)
+    out_perm = np.zeros((cfg.num_particles, n), np.int64)
+    mode = {"global-max": 0, "pick-column": 1, "second-target": 2}[cf.sx_mode]
+    orc.aggregate_many(x, np.ascontiguousarray(got), mode, cf.depth, draws[:, 2:], out_mat, out_perm)
+    assert np.array_equal(out_perm, st.perms)
+    cost = np.zeros(cfg.num_particles, np.int64)
+    orc.cost_many(out_perm, inst.flow, inst.distance, cost)
+    assert np.array_equal(cost, st.cost)
+    if st.d_vcol is not None:
+        _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
+
+
+def test_fp32_lazy_toggle_and_graphs(golden_instances):
+    """Leaving the lazy layout materialises v; re-entering starts from a full
+    pass; graph replay (step_many) keeps the column state identical to eager
+    steps."""
+    inst = golden_instances["tai30"]
+    cfg = qsb.SolverConfig(swarms=4, swarm_size=25, seed=5, precision="fp32",
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    a = qsb.init_population(cfg, inst)
+    b = qsb.init_population(cfg, inst)
+    for _ in range(6):
+        qsb.step(a, inst, cfg)
+    qsb.step_many(b, inst, cfg, 6)
+    assert a.d_vcol.cpu().numpy().tobytes() == b.d_vcol.cpu().numpy().tobytes()
+    assert a.d_V.cpu().numpy().tobytes() == b.d_V.cpu().numpy().tobytes()
+    v_before = a.V
+    a.set_lazy_scale(False)
+    assert a.d_vcol is None
+    assert np.allclose(a.V, v_before, rtol=1e-6, atol=0)
+    qsb.step(a, inst, cfg)
+    a.set_lazy_scale(True)
+    qsb.step(a, inst, cfg)
+    qsb.step(a, inst, cfg)
+    _lazy_state_checks(a, inst.n)
+
+
 @pytest.mark.parametrize("name,steps,c1", [("tai50", 1, 0.8), ("tai50", 7, 0.8),
                                            ("tai50", 45, 0.8), ("tai30", 30, 0.6),
                                            ("chr12a", 50, 0.9)])
