@@ -150,6 +150,8 @@ struct MigArgs {
   int mode;              // 0 fused (plan+apply), 1 plan+pack, 2 apply from rec
 };
 
+constexpr int MIG_SORT_MAX = 8192;   // swarms sorted in shared memory (larger m: rank counting)
+
 // Stable ascending rank of every swarm cost (np.argsort(kind="stable")),
 // then rank k donates to rank m-1-k (migration.py:81-90).
 template <typename CT>
@@ -196,14 +198,44 @@ __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
   const CT* allc = reinterpret_cast<const CT*>(a.all_pg_cost);
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) sc[i] = allc[i];
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const CT ci = sc[i];
-    int64_t r = 0;
-    for (int64_t j = 0; j < m; ++j) {
-      const CT cj = sc[j];
-      r += (cj < ci) || (cj == ci && j < i);
+  const int mi = (int)m;
+  const int p2 = mi <= 1 ? 1 : 1 << (32 - __clz(mi - 1));
+  if (p2 <= MIG_SORT_MAX) {
+    // stable ascending order (np.argsort kind="stable") by a bitonic sort of
+    // (cost, index) keys in shared memory, padded to a power of two
+    CT* kc = reinterpret_cast<CT*>(order + align_up((size_t)p2, 4));   // ki = order: p2 entries
+    int32_t* ki = order;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+      kc[i] = i < mi ? sc[i] : ct_max<CT>();
+      ki[i] = i < mi ? i : INT_MAX;
     }
-    order[r] = (int32_t)i;
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+          const int j = i ^ stride;
+          if (j <= i) continue;
+          const CT ci = kc[i], cj = kc[j];
+          const int ii = ki[i], ij = ki[j];
+          const bool gt = ci > cj || (ci == cj && ii > ij);
+          if (gt == ((i & size) == 0)) { kc[i] = cj; kc[j] = ci; ki[i] = ij; ki[j] = ii; }
+        }
+        __syncthreads();
+      }
+    }
+  } else {
+    // large m: stable rank of each swarm cost, one warp per swarm
+    const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < mi; i += nwarp) {
+      const CT ci = sc[i];
+      unsigned r = 0;
+      for (int j = lane; j < mi; j += 32) {
+        const CT cj = sc[j];
+        r += (cj < ci) || (cj == ci && j < i);
+      }
+      r = __reduce_add_sync(0xffffffffu, r);
+      if (lane == 0) order[r] = i;
+    }
   }
   __syncthreads();
   const int32_t* picks = a.picks + row * a.d;
@@ -225,20 +257,32 @@ __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
       e[5] = src_local ? (double)lcost[lp] : 0.0;   // multi-device: filled by the host
     }
     if (a.mode == 0) {
-      // one device owns everything: donor read + swarm-best write in place
-      pgc[dst] = lcost[lp];
-      for (int q = 0; q < n; ++q) a.pg_perm[dst * n + q] = a.perm[lp * n + q];
+      pgc[dst] = lcost[lp];   // one device owns everything: swarm-best cost in place
     } else if (a.rec) {
       int64_t* r = a.rec + (int64_t)k * (n + 1);
       if (src_local) {
         if constexpr (std::is_floating_point<CT>::value) r[0] = __double_as_longlong(lcost[lp]);
         else r[0] = (int64_t)lcost[lp];
-        for (int q = 0; q < n; ++q) r[1 + q] = a.perm[lp * n + q];
       } else {
-        for (int q = 0; q <= n; ++q) r[q] = 0;
+        r[0] = 0;
       }
     }
     (void)dst_local;
+  }
+  // the donor permutations, all (event, facility) pairs across the block
+  if (a.mode == 0 || a.rec) {
+    const int64_t dn = (int64_t)a.d * n;
+    for (int64_t e = threadIdx.x; e < dn; e += blockDim.x) {
+      const int k = (int)(e / n), q = (int)(e - (int64_t)k * n);
+      const int64_t src = order[k];
+      const int64_t lp = src * a.S + picks[k] - a.m0 * a.S;
+      const bool src_local = src >= a.m0 && src < a.m0 + a.m_local;
+      if (a.mode == 0) {
+        a.pg_perm[(int64_t)order[m - 1 - k] * n + q] = a.perm[lp * n + q];
+      } else {
+        a.rec[(int64_t)k * (n + 1) + 1 + q] = src_local ? (int64_t)a.perm[lp * n + q] : 0;
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0 && a.log && (*a.log_count / a.d) < a.log_rows) *a.log_count += a.d;

@@ -335,7 +335,10 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
   if (a.mode == 0 && (a.m0 != 0 || a.m_local != a.m)) return QSB_EINVAL;
   if (a.mode == 2 && !a.rec) return QSB_EINVAL;
   const size_t csz = st->cost_dtype == QSB_F64 ? 8 : 8;
-  const size_t smem = align_up((size_t)a.m * csz, 16) + (size_t)a.m * 4;
+  size_t p2 = 1;
+  while (p2 < (size_t)a.m) p2 <<= 1;
+  const size_t smem = align_up((size_t)a.m * csz, 16) +
+                      (p2 <= (size_t)MIG_SORT_MAX ? align_up(p2, 4) * 4 + p2 * 8 : (size_t)a.m * 4);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   if (st->cost_dtype == QSB_I64) {
