@@ -194,6 +194,7 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream);
  * (use it with qsb_step_phases without QSB_PHASE_PBEST). */
 #define QSB_TWOOPT_PBEST 1
 #define QSB_TWOOPT_SYMMETRIC 2   /* caller-checked: flow and distance symmetric, < 2^16 */
+#define QSB_TWOOPT_BYTES 4       /* caller-checked: entries < 256 and n*max(F)*max(D) < 2^31 */
 int qsb_twoopt(const qsb_state* st, const qsb_instance* inst, int32_t passes, int32_t flags,
                void* stream);
 

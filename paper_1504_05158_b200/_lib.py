@@ -22,6 +22,7 @@ PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 
 HINT_V_BOUNDED = 1
 HINT_COST_CURRENT = 2
 TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
+TWOOPT_BYTES = 4
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V
 
 _vp = ctypes.c_void_p

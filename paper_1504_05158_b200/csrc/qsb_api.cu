@@ -157,8 +157,39 @@ static int launch_twoopt(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
+// byte-matrix dp4a kernel (symmetric, entries < 256, n * max * max < 2^31)
+template <int NT>
+static int launch_twoopt_dp4a(TwoOptArgs t, cudaStream_t s) {
+  const int nr = (t.n + 3) / 4 * 4;
+  int ldn = nr;
+  if (((ldn / 4) & 1) == 0) ldn += 4;     // odd word stride: rows in distinct banks
+  t.ldn = ldn;
+  const size_t smem = 3 * (size_t)nr * ldn + 2 * (size_t)nr * 4 + 8 + (NT / 32) * 12 + 16;
+  if (smem > smem_optin()) return QSB_EUNSUPPORTED;
+  auto fn = twoopt_dp4a_kernel<NT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  int bps = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, NT, smem);
+  if (bps < 1) bps = 1;
+  const int64_t cap = (int64_t)num_sms() * bps;
+  const int grid = (int)(t.P < cap ? t.P : cap);
+  if (grid <= 0) return QSB_OK;
+  fn<<<grid, NT, smem, s>>>(t);
+  return launch_status();
+}
+
 template <typename MT>
-static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s) {
+static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = false) {
+  if constexpr (sizeof(MT) == 2) {
+    if (bytes && t.sym) {
+      const int rc = t.n <= 64 ? launch_twoopt_dp4a<128>(t, s)
+                   : (t.n <= 128 ? launch_twoopt_dp4a<256>(t, s) : launch_twoopt_dp4a<512>(t, s));
+      if (rc != QSB_EUNSUPPORTED) return rc;
+    }
+  }
   return t.n <= 64 ? launch_twoopt<MT, 128>(t, s) : launch_twoopt<MT, 256>(t, s);
 }
 
@@ -471,7 +502,8 @@ int qsb_twoopt(const qsb_state* st, const qsb_instance* inst, int32_t passes, in
   t.D = inst->distance;
   if (t.P == 0 || (passes == 0 && !t.do_pbest)) return QSB_OK;
   if (t.do_pbest && (!t.pl_perm || !t.pl_cost || !t.improved)) return QSB_EINVAL;
-  if (inst->mat_dtype == QSB_U16) return dispatch_twoopt<uint16_t>(t, (cudaStream_t)stream);
+  if (inst->mat_dtype == QSB_U16)
+    return dispatch_twoopt<uint16_t>(t, (cudaStream_t)stream, (flags & QSB_TWOOPT_BYTES) != 0);
   return dispatch_twoopt<int64_t>(t, (cudaStream_t)stream);
 }
 
@@ -695,6 +727,7 @@ int qsb_twoopt_many(int64_t* perms, const int64_t* flow, const int64_t* distance
   int64_t mx = 0;
   for (int64_t i = 0; i < nn; ++i) { if (flow[i] > mx) mx = flow[i]; if (distance[i] > mx) mx = distance[i]; }
   if (mx >= (1 << 16)) sym = false;
+  const bool bytes = mx < 256 && (double)n * (double)mx * (double)mx < 2147483648.0;
   QSB_TRY(h.b[6].ensure(P * n * 2 + P * 8 + 16));
   QSB_TRY(h.b[7].ensure(2 * nn * 8));
   const bool narrow = mx < (1 << 16);   // uint16 device matrices when exact
@@ -718,7 +751,7 @@ int qsb_twoopt_many(int64_t* perms, const int64_t* flow, const int64_t* distance
   t.perm = dp; t.cost = dc;
   t.F = h.b[7].p;
   t.D = (char*)h.b[7].p + nn * (narrow ? 2 : 8);
-  if (narrow) QSB_TRY(dispatch_twoopt<uint16_t>(t, s));
+  if (narrow) QSB_TRY(dispatch_twoopt<uint16_t>(t, s, bytes));
   else QSB_TRY(dispatch_twoopt<int64_t>(t, s));
   QSB_CUDA(cudaMemcpyAsync(hp.data(), dp, P * n * 2, cudaMemcpyDeviceToHost, s));
   QSB_CUDA(cudaMemcpyAsync(costs, dc, P * 8, cudaMemcpyDeviceToHost, s));

@@ -21,6 +21,7 @@ namespace qsb {
 
 struct TwoOptArgs {
   int n;
+  int ldn;          // byte-matrix row stride (dp4a kernel)
   int64_t P;
   int passes;
   int sym;          // F and D symmetric (halves the delta sweep)
@@ -166,6 +167,166 @@ __global__ void __launch_bounds__(NT) twoopt_kernel(const TwoOptArgs a) {
     for (int i = threadIdx.x; i < n; i += NT) a.perm[p * n + i] = (int16_t)sp[i];
     if (a.do_pbest) {
       // one thread decides (strict <, engine.py:211), then all copy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const bool imp = (int64_t)cost < a.pl_cost[p];
+        if (imp) a.pl_cost[p] = (int64_t)cost;
+        a.improved[p] = imp ? 1 : 0;
+        s_move = imp;
+      }
+      __syncthreads();
+      if (s_move)
+        for (int i = threadIdx.x; i < n; i += NT) a.pl_perm[p * n + i] = (int16_t)sp[i];
+    }
+    if (threadIdx.x == 0) a.cost[p] = (int64_t)cost;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// 2-opt for symmetric instances with byte-sized entries (n * max(F) * max(D)
+// < 2^31), as packed 4-way byte dot products.  For symmetric F and D the
+// permuted distance matrix P = D[p][p] is symmetric and
+//   sum_{k != r,s} (F_kr - F_ks)(P_ks - P_kr)
+//     = G[r][s] + G[s][r] - G[r][r] - G[s][s] - T_r - T_s,
+//   G[a][b] = sum_k F[a][k] P[b][k]   (rows: contiguous k),
+//   T_r = (F_rr - F_rs)(P_rs - P_rr),  T_s = (F_sr - F_ss)(P_ss - P_sr),
+// so delta(r, s) = (F_rr - F_ss)(P_ss - P_rr) + 2 * that sum -- the value
+// twoopt_kernel's symmetric sweep computes, exact in int64 (G < 2^31).
+// Each thread owns a 4 x 4 block pair (rows r0.., s0..) of the upper
+// triangle and accumulates G[r][s] and G[s][r] with __dp4a over 4-byte row
+// words (row stride ldn = 4 x odd words, so the rows a warp reads sit in
+// distinct banks).  F, D and P are byte matrices in shared memory.
+template <int NT>
+__global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  const int n = a.n;
+  const int ldn = a.ldn;
+  const int ldw = ldn >> 2;
+  const int nb = (n + 3) >> 2;        // 4-row blocks
+  const int nr = nb * 4;              // rows incl. zero padding
+  uint8_t* F8 = tsm;
+  uint8_t* D8 = F8 + (size_t)nr * ldn;
+  uint8_t* P8 = D8 + (size_t)nr * ldn;
+  int* sp = reinterpret_cast<int*>(P8 + (size_t)nr * ldn);
+  int* gd = sp + nr;
+  int64_t* rd = reinterpret_cast<int64_t*>(gd + nr + (nr & 1));
+  int* rq = reinterpret_cast<int*>(rd + NT / 32);
+  __shared__ int s_move;
+  const unsigned* F32 = reinterpret_cast<const unsigned*>(F8);
+  const unsigned* P32 = reinterpret_cast<const unsigned*>(P8);
+  const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
+  const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < nr * ldn; e += NT) {
+    const int r = e / ldn, c = e - r * ldn;
+    const bool in = r < n && c < n;
+    F8[e] = in ? (uint8_t)gF[r * n + c] : 0;
+    D8[e] = in ? (uint8_t)gD[r * n + c] : 0;
+    P8[e] = 0;
+  }
+  const int nbp = nb * (nb + 1) / 2;
+  for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr; i += NT) sp[i] = i < n ? a.perm[p * n + i] : 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * ldn; e += NT) {
+      const int r = e / ldn, c = e - r * ldn;
+      if (c < n) P8[e] = D8[sp[r] * ldn + sp[c]];
+    }
+    __syncthreads();
+    uint64_t cost = (uint64_t)a.cost[p];
+    for (int pass = 0; pass < a.passes; ++pass) {
+      // G[r][r] for every row
+      for (int r = threadIdx.x; r < n; r += NT) {
+        unsigned acc = 0;
+        for (int w = 0; w < ldw; ++w) acc = __dp4a(F32[r * ldw + w], P32[r * ldw + w], acc);
+        gd[r] = (int)acc;
+      }
+      __syncthreads();
+      int64_t best = INT64_MAX;
+      int bq = INT_MAX;
+      for (int bp = threadIdx.x; bp < nbp; bp += NT) {
+        // block pair (bi <= bj) from its upper-triangle rank
+        int bi = (int)((2.0f * nb + 1.0f - sqrtf((2.0f * nb + 1.0f) * (2.0f * nb + 1.0f) - 8.0f * bp)) * 0.5f);
+        bi = max(0, min(bi, nb - 1));
+        while (bi > 0 && bi * nb - bi * (bi - 1) / 2 > bp) --bi;
+        while (bi + 1 < nb && (bi + 1) * nb - (bi + 1) * bi / 2 <= bp) ++bi;
+        const int bj = bi + bp - (bi * nb - bi * (bi - 1) / 2);
+        const int r0 = 4 * bi, s0 = 4 * bj;
+        unsigned gA[4][4], gB[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) { gA[x][y] = 0; gB[x][y] = 0; }
+        const unsigned* fr = F32 + r0 * ldw;
+        const unsigned* fs = F32 + s0 * ldw;
+        const unsigned* pr = P32 + r0 * ldw;
+        const unsigned* ps = P32 + s0 * ldw;
+#pragma unroll 2
+        for (int w = 0; w < ldw; ++w) {
+          unsigned f_r[4], f_s[4], p_r[4], p_s[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            f_r[x] = fr[x * ldw + w]; p_r[x] = pr[x * ldw + w];
+            f_s[x] = fs[x * ldw + w]; p_s[x] = ps[x * ldw + w];
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              gA[x][y] = __dp4a(f_r[x], p_s[y], gA[x][y]);   // G[r][s]
+              gB[x][y] = __dp4a(f_s[y], p_r[x], gB[x][y]);   // G[s][r]
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const int r = r0 + x, s = s0 + y;
+            if (r >= s || s >= n) continue;
+            const int64_t Frr = F8[r * ldn + r], Fss = F8[s * ldn + s], Frs = F8[r * ldn + s];
+            const int64_t Prr = P8[r * ldn + r], Pss = P8[s * ldn + s], Prs = P8[r * ldn + s];
+            const int64_t sum = (int64_t)gA[x][y] + (int64_t)gB[x][y] - gd[r] - gd[s]
+                                - (Frr - Frs) * (Prs - Prr) - (Frs - Fss) * (Pss - Prs);
+            const int64_t dd = (Frr - Fss) * (Pss - Prr) + 2 * sum;
+            const int q = r * n - r * (r + 1) / 2 + (s - r - 1);
+            if (dd < best || (dd == best && q < bq)) { best = dd; bq = q; }
+          }
+      }
+      // lexicographic (delta, q) minimum over the CTA
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      if (lane == 0) { rd[warp] = best; rq[warp] = bq; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < NT / 32; ++w)
+          if (rd[w] < rd[0] || (rd[w] == rd[0] && rq[w] < rq[0])) { rd[0] = rd[w]; rq[0] = rq[w]; }
+        s_move = (rq[0] != INT_MAX && rd[0] < 0) ? rq[0] : -1;
+      }
+      __syncthreads();
+      const int mq = s_move;
+      if (mq < 0) break;
+      cost += (uint64_t)rd[0];
+      int r, s;
+      unrank_pair(mq, n, r, s);
+      // swap facilities r and s: rows r, s then columns r, s of P
+      for (int j = threadIdx.x; j < n; j += NT) {
+        const uint8_t t = P8[r * ldn + j]; P8[r * ldn + j] = P8[s * ldn + j]; P8[s * ldn + j] = t;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += NT) {
+        const uint8_t t = P8[i * ldn + r]; P8[i * ldn + r] = P8[i * ldn + s]; P8[i * ldn + s] = t;
+      }
+      if (threadIdx.x == 0) { const int t = sp[r]; sp[r] = sp[s]; sp[s] = t; }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += NT) a.perm[p * n + i] = (int16_t)sp[i];
+    if (a.do_pbest) {
       __syncthreads();
       if (threadIdx.x == 0) {
         const bool imp = (int64_t)cost < a.pl_cost[p];

@@ -324,6 +324,9 @@ class _Runtime:
         self.mat_code = code
         fa, da = np.asarray(instance.flow), np.asarray(instance.distance)
         self.symmetric = bool(code == _lib.U16 and (fa == fa.T).all() and (da == da.T).all())
+        # byte-sized entries with int32-safe sums: the 2-opt dp4a kernel
+        mf, md = (int(fa.max()), int(da.max())) if fa.size else (0, 0)
+        self.twoopt_bytes = bool(code == _lib.U16 and max(mf, md) < 256 and state.n * mf * md < 2**31)
         self.key = (id(instance), config.coefficients, config.seed)
         c = config.coefficients
         self.coeffs = _lib.QsbCoeffs(c.c1, c.c2, c.c3, c.v_max, int(c.sv_mode == "norm"),
@@ -571,7 +574,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     if timer is not None:
         timer.after(stream)
     if passes:
-        tf = _lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+        tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+              | (_lib.TWOOPT_BYTES if rt.twoopt_bytes else 0))
         _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, stream)
         state.launches += 1
     _lib.call("qsb_best_update", cs, stream)
@@ -652,7 +656,8 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
             mig.status = ms.status.data_ptr()
         passes = config.two_opt_passes
         flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
-        tf = _lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+        tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+              | (_lib.TWOOPT_BYTES if rt.twoopt_bytes else 0))
         cs_a = state.c_state()
         cs_b = _lib.QsbState.from_buffer_copy(cs_a)
         cs_b.perm, cs_b.perm_new = cs_a.perm_new, cs_a.perm
