@@ -161,10 +161,10 @@ static int launch_twoopt(TwoOptArgs t, cudaStream_t s) {
 template <int NT>
 static int launch_twoopt_dp4a(TwoOptArgs t, cudaStream_t s) {
   const int nr = (t.n + 3) / 4 * 4;
-  int ldn = nr;
-  if (((ldn / 4) & 1) == 0) ldn += 4;     // odd word stride: rows in distinct banks
-  t.ldn = ldn;
-  const size_t smem = 3 * (size_t)nr * ldn + 2 * (size_t)nr * 4 + 8 + (NT / 32) * 12 + 16;
+  int ldw = nr / 4;                       // 16-byte chunks per 4-row block
+  if ((ldw & 1) == 0) ldw += 1;           // odd: consecutive blocks in distinct banks
+  t.ldn = 4 * ldw;
+  const size_t smem = 3 * (size_t)(nr / 4) * ldw * 16 + 2 * (size_t)nr * 4 + 8 + (NT / 32) * 12 + 16;
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
   auto fn = twoopt_dp4a_kernel<NT>;
   if (smem > 48 * 1024) {
@@ -185,7 +185,8 @@ template <typename MT>
 static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = false) {
   if constexpr (sizeof(MT) == 2) {
     if (bytes && t.sym) {
-      const int rc = t.n <= 64 ? launch_twoopt_dp4a<128>(t, s)
+      const int rc = t.n <= 32 ? launch_twoopt_dp4a<64>(t, s)
+                   : t.n <= 64 ? launch_twoopt_dp4a<128>(t, s)
                    : (t.n <= 128 ? launch_twoopt_dp4a<256>(t, s) : launch_twoopt_dp4a<512>(t, s));
       if (rc != QSB_EUNSUPPORTED) return rc;
     }

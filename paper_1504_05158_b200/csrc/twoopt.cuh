@@ -194,53 +194,66 @@ __global__ void __launch_bounds__(NT) twoopt_kernel(const TwoOptArgs a) {
 // so delta(r, s) = (F_rr - F_ss)(P_ss - P_rr) + 2 * that sum -- the value
 // twoopt_kernel's symmetric sweep computes, exact in int64 (G < 2^31).
 // Each thread owns a 4 x 4 block pair (rows r0.., s0..) of the upper
-// triangle and accumulates G[r][s] and G[s][r] with __dp4a over 4-byte row
-// words (row stride ldn = 4 x odd words, so the rows a warp reads sit in
-// distinct banks).  F, D and P are byte matrices in shared memory.
+// triangle and accumulates G[r][s] and G[s][r] with __dp4a.  The byte
+// matrices live in shared memory in a 4-row interleaved layout: the four
+// rows of a block share 16-byte chunks, so one 128-bit load fetches word w
+// of all four rows, and an odd chunk stride per block keeps the loads of
+// consecutive blocks in distinct banks.
+__device__ __forceinline__ int bidx(int r, int c, int ldw) {
+  return ((((r >> 2) * ldw + (c >> 2)) << 4) | ((r & 3) << 2) | (c & 3));
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
   extern __shared__ __align__(16) unsigned char tsm[];
   const int n = a.n;
-  const int ldn = a.ldn;
-  const int ldw = ldn >> 2;
-  const int nb = (n + 3) >> 2;        // 4-row blocks
-  const int nr = nb * 4;              // rows incl. zero padding
+  const int ldw = a.ldn >> 2;          // 16-byte chunks per 4-row block (odd)
+  const int nb = (n + 3) >> 2;         // 4-row blocks
+  const int nr = nb * 4;
+  const size_t mbytes = (size_t)nb * ldw * 16;
   uint8_t* F8 = tsm;
-  uint8_t* D8 = F8 + (size_t)nr * ldn;
-  uint8_t* P8 = D8 + (size_t)nr * ldn;
-  int* sp = reinterpret_cast<int*>(P8 + (size_t)nr * ldn);
+  uint8_t* D8 = F8 + mbytes;
+  uint8_t* P8 = D8 + mbytes;
+  int* sp = reinterpret_cast<int*>(P8 + mbytes);
   int* gd = sp + nr;
   int64_t* rd = reinterpret_cast<int64_t*>(gd + nr + (nr & 1));
   int* rq = reinterpret_cast<int*>(rd + NT / 32);
   __shared__ int s_move;
-  const unsigned* F32 = reinterpret_cast<const unsigned*>(F8);
-  const unsigned* P32 = reinterpret_cast<const unsigned*>(P8);
+  const uint4* F128 = reinterpret_cast<const uint4*>(F8);
+  const uint4* P128 = reinterpret_cast<const uint4*>(P8);
   const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
   const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < nr * ldn; e += NT) {
-    const int r = e / ldn, c = e - r * ldn;
+  const int ncols = ldw * 4;
+  for (int e = threadIdx.x; e < nr * ncols; e += NT) {
+    const int r = e / ncols, c = e - r * ncols;
     const bool in = r < n && c < n;
-    F8[e] = in ? (uint8_t)gF[r * n + c] : 0;
-    D8[e] = in ? (uint8_t)gD[r * n + c] : 0;
-    P8[e] = 0;
+    const int i = bidx(r, c, ldw);
+    F8[i] = in ? (uint8_t)gF[r * n + c] : 0;
+    D8[i] = in ? (uint8_t)gD[r * n + c] : 0;
+    P8[i] = 0;
   }
   const int nbp = nb * (nb + 1) / 2;
   for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
     __syncthreads();
     for (int i = threadIdx.x; i < nr; i += NT) sp[i] = i < n ? a.perm[p * n + i] : 0;
     __syncthreads();
-    for (int e = threadIdx.x; e < n * ldn; e += NT) {
-      const int r = e / ldn, c = e - r * ldn;
-      if (c < n) P8[e] = D8[sp[r] * ldn + sp[c]];
+    for (int e = threadIdx.x; e < n * n; e += NT) {
+      const int r = e / n, c = e - r * n;
+      P8[bidx(r, c, ldw)] = D8[bidx(sp[r], sp[c], ldw)];
     }
     __syncthreads();
     uint64_t cost = (uint64_t)a.cost[p];
     for (int pass = 0; pass < a.passes; ++pass) {
       // G[r][r] for every row
       for (int r = threadIdx.x; r < n; r += NT) {
+        const unsigned* F32 = reinterpret_cast<const unsigned*>(F8);
+        const unsigned* P32 = reinterpret_cast<const unsigned*>(P8);
         unsigned acc = 0;
-        for (int w = 0; w < ldw; ++w) acc = __dp4a(F32[r * ldw + w], P32[r * ldw + w], acc);
+        for (int w = 0; w < ldw; ++w) {
+          const int wi = (((r >> 2) * ldw + w) << 2) | (r & 3);
+          acc = __dp4a(F32[wi], P32[wi], acc);
+        }
         gd[r] = (int)acc;
       }
       __syncthreads();
@@ -253,24 +266,22 @@ __global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
         while (bi > 0 && bi * nb - bi * (bi - 1) / 2 > bp) --bi;
         while (bi + 1 < nb && (bi + 1) * nb - (bi + 1) * bi / 2 <= bp) ++bi;
         const int bj = bi + bp - (bi * nb - bi * (bi - 1) / 2);
-        const int r0 = 4 * bi, s0 = 4 * bj;
         unsigned gA[4][4], gB[4][4];
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 4; ++y) { gA[x][y] = 0; gB[x][y] = 0; }
-        const unsigned* fr = F32 + r0 * ldw;
-        const unsigned* fs = F32 + s0 * ldw;
-        const unsigned* pr = P32 + r0 * ldw;
-        const unsigned* ps = P32 + s0 * ldw;
+        const uint4* fr = F128 + bi * ldw;
+        const uint4* pr = P128 + bi * ldw;
+        const uint4* fs = F128 + bj * ldw;
+        const uint4* ps = P128 + bj * ldw;
 #pragma unroll 2
         for (int w = 0; w < ldw; ++w) {
-          unsigned f_r[4], f_s[4], p_r[4], p_s[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            f_r[x] = fr[x * ldw + w]; p_r[x] = pr[x * ldw + w];
-            f_s[x] = fs[x * ldw + w]; p_s[x] = ps[x * ldw + w];
-          }
+          const uint4 a_fr = fr[w], a_pr = pr[w], a_fs = fs[w], a_ps = ps[w];
+          const unsigned f_r[4] = {a_fr.x, a_fr.y, a_fr.z, a_fr.w};
+          const unsigned p_r[4] = {a_pr.x, a_pr.y, a_pr.z, a_pr.w};
+          const unsigned f_s[4] = {a_fs.x, a_fs.y, a_fs.z, a_fs.w};
+          const unsigned p_s[4] = {a_ps.x, a_ps.y, a_ps.z, a_ps.w};
 #pragma unroll
           for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -279,14 +290,15 @@ __global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
               gB[x][y] = __dp4a(f_s[y], p_r[x], gB[x][y]);   // G[s][r]
             }
         }
+        const int r0 = 4 * bi, s0 = 4 * bj;
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 4; ++y) {
             const int r = r0 + x, s = s0 + y;
             if (r >= s || s >= n) continue;
-            const int64_t Frr = F8[r * ldn + r], Fss = F8[s * ldn + s], Frs = F8[r * ldn + s];
-            const int64_t Prr = P8[r * ldn + r], Pss = P8[s * ldn + s], Prs = P8[r * ldn + s];
+            const int64_t Frr = F8[bidx(r, r, ldw)], Fss = F8[bidx(s, s, ldw)], Frs = F8[bidx(r, s, ldw)];
+            const int64_t Prr = P8[bidx(r, r, ldw)], Pss = P8[bidx(s, s, ldw)], Prs = P8[bidx(r, s, ldw)];
             const int64_t sum = (int64_t)gA[x][y] + (int64_t)gB[x][y] - gd[r] - gd[s]
                                 - (Frr - Frs) * (Prs - Prr) - (Frs - Fss) * (Pss - Prs);
             const int64_t dd = (Frr - Fss) * (Pss - Prr) + 2 * sum;
@@ -316,11 +328,13 @@ __global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
       unrank_pair(mq, n, r, s);
       // swap facilities r and s: rows r, s then columns r, s of P
       for (int j = threadIdx.x; j < n; j += NT) {
-        const uint8_t t = P8[r * ldn + j]; P8[r * ldn + j] = P8[s * ldn + j]; P8[s * ldn + j] = t;
+        const int ir = bidx(r, j, ldw), is = bidx(s, j, ldw);
+        const uint8_t t = P8[ir]; P8[ir] = P8[is]; P8[is] = t;
       }
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += NT) {
-        const uint8_t t = P8[i * ldn + r]; P8[i * ldn + r] = P8[i * ldn + s]; P8[i * ldn + s] = t;
+        const int ir = bidx(i, r, ldw), is = bidx(i, s, ldw);
+        const uint8_t t = P8[ir]; P8[ir] = P8[is]; P8[is] = t;
       }
       if (threadIdx.x == 0) { const int t = sp[r]; sp[r] = sp[s]; sp[s] = t; }
       __syncthreads();
