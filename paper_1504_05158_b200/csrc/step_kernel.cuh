@@ -1837,7 +1837,7 @@ step_kernel(const StepArgs a) {
       //                + sum_{i not in C, j in C} F[i][j] (D'[i][j] - D[i][j])
       // with D[i][j] = D[p_i][p_j].  Exact in int64 (mod 2^64, as the full
       // sum).  Needs cost[p] == goal(perm[p]) on entry (host guarantee).
-      if (do_cost && a.cost_incremental) {
+      if (do_cost && a.cost_incremental && sizeof(MT) <= 2 && a.acc32 && n >= 8) {
         Sync::sync();
         const int c0 = lane, c1 = lane + 32;
         const bool m0 = c0 < n && sc.sperm[c0] != sc.szr[c0];
@@ -1860,17 +1860,17 @@ step_kernel(const StepArgs a) {
               const int i = h * 32 + __ffs(b) - 1;
               b &= b - 1;
               const int pin = sc.sperm[i], pio = sc.szr[i];
-              // row i of the changed facilities, every column (owned by lanes)
+              // n max(F) max(D) < 2^32, n >= 8 (host / launch checked): every
+              // term F (D' - D) and this facility's <= 2 * CPL terms per lane
+              // fit int32
+              int part = 0;
 #pragma unroll
               for (int kk = 0; kk < CPL; ++kk)
                 if (col[kk] < n)
-                  acc += (uint64_t)cF[i * n + col[kk]] *
-                         (uint64_t)((int64_t)cD[pin * n + pjn[kk]] - (int64_t)cD[pio * n + pjo[kk]]);
-              // column i, rows that did not move (lanes own rows lane, lane+32)
-              if (c0 < n && !m0)
-                acc += (uint64_t)cF[c0 * n + i] * (uint64_t)((int64_t)cD[ro0 * n + pin] - (int64_t)cD[ro0 * n + pio]);
-              if (c1 < n && !m1)
-                acc += (uint64_t)cF[c1 * n + i] * (uint64_t)((int64_t)cD[ro1 * n + pin] - (int64_t)cD[ro1 * n + pio]);
+                  part += (int)cF[i * n + col[kk]] * ((int)cD[pin * n + pjn[kk]] - (int)cD[pio * n + pjo[kk]]);
+              if (c0 < n && !m0) part += (int)cF[c0 * n + i] * ((int)cD[ro0 * n + pin] - (int)cD[ro0 * n + pio]);
+              if (c1 < n && !m1) part += (int)cF[c1 * n + i] * ((int)cD[ro1 * n + pin] - (int)cD[ro1 * n + pio]);
+              acc += (uint64_t)(int64_t)part;
             }
           }
           const int64_t delta = warp_sum_i64((int64_t)acc);
