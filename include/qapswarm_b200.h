@@ -132,6 +132,9 @@ typedef struct qsb_coeffs {
  * steps), so the new goal may be computed incrementally from the facilities
  * that moved (integral instances). */
 #define QSB_HINT_COST_CURRENT 2
+/* flow and distance are symmetric (integral instances): the incremental goal
+ * counts the unmoved rows' column terms through the moved rows' row terms. */
+#define QSB_HINT_SYMMETRIC 4
 
 /* One migration event (migration.migrate, migration.py:55-86). */
 typedef struct qsb_migration {

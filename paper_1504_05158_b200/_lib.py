@@ -21,6 +21,7 @@ F32, F64, I64, U16 = 1, 2, 3, 4
 PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 4, 8, 16
 HINT_V_BOUNDED = 1
 HINT_COST_CURRENT = 2
+HINT_SYMMETRIC = 4
 TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
 TWOOPT_BYTES = 4
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V

@@ -255,6 +255,7 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.acc32 = inst ? inst->acc32 : 0;
   a.v_bounded = (co->hints & QSB_HINT_V_BOUNDED) ? 1 : 0;
   a.cost_incremental = (co->hints & QSB_HINT_COST_CURRENT) ? 1 : 0;
+  a.symmetric = (co->hints & QSB_HINT_SYMMETRIC) ? 1 : 0;
   a.vcol = st->v_dtype == QSB_F32 ? st->vcol : nullptr;
   a.vcstride = (st->n + 3) / 4 * 4;
 }

@@ -70,6 +70,7 @@ struct StepArgs {
   int v_bounded;             // host guarantee: |c1 * v| <= v_max for every stored v
   int acc32;                 // host guarantee: n * max(F) * max(D) < 2^32
   int cost_incremental;      // host guarantee: cost[p] == goal(perm[p]) on entry
+  int symmetric;             // host guarantee: F and D symmetric (integral instances)
   unsigned int* work;        // optional zeroed counter: dynamic particle scheduling
   float* vcol;               // fp32 lazily scaled layout: (P, 4, vcstride) column state, or null
   int vcstride;
@@ -1853,6 +1854,9 @@ step_kernel(const StepArgs a) {
             pjo[kk] = col[kk] < n ? sc.szr[col[kk]] : 0;
           }
           const int ro0 = c0 < n ? sc.szr[c0] : 0, ro1 = c1 < n ? sc.szr[c1] : 0;
+          int wsym[CPL];
+#pragma unroll
+          for (int kk = 0; kk < CPL; ++kk) wsym[kk] = (a.symmetric && !(kk == 0 ? m0 : m1)) ? 2 : 1;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             unsigned b = ch[h];
@@ -1863,13 +1867,18 @@ step_kernel(const StepArgs a) {
               // n max(F) max(D) < 2^32, n >= 8 (host / launch checked): every
               // term F (D' - D) and this facility's <= 2 * CPL terms per lane
               // fit int32
+              // (F, D symmetric: an unmoved row's column-i term equals its
+              // row-i term, which then counts twice)
               int part = 0;
 #pragma unroll
               for (int kk = 0; kk < CPL; ++kk)
                 if (col[kk] < n)
-                  part += (int)cF[i * n + col[kk]] * ((int)cD[pin * n + pjn[kk]] - (int)cD[pio * n + pjo[kk]]);
-              if (c0 < n && !m0) part += (int)cF[c0 * n + i] * ((int)cD[ro0 * n + pin] - (int)cD[ro0 * n + pio]);
-              if (c1 < n && !m1) part += (int)cF[c1 * n + i] * ((int)cD[ro1 * n + pin] - (int)cD[ro1 * n + pio]);
+                  part += wsym[kk] * (int)cF[i * n + col[kk]] *
+                          ((int)cD[pin * n + pjn[kk]] - (int)cD[pio * n + pjo[kk]]);
+              if (!a.symmetric) {
+                if (c0 < n && !m0) part += (int)cF[c0 * n + i] * ((int)cD[ro0 * n + pin] - (int)cD[ro0 * n + pio]);
+                if (c1 < n && !m1) part += (int)cF[c1 * n + i] * ((int)cD[ro1 * n + pin] - (int)cD[ro1 * n + pio]);
+              }
               acc += (uint64_t)(int64_t)part;
             }
           }

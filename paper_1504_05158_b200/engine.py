@@ -323,7 +323,9 @@ class _Runtime:
                                      acc32, 0)
         self.mat_code = code
         fa, da = np.asarray(instance.flow), np.asarray(instance.distance)
-        self.symmetric = bool(code == _lib.U16 and (fa == fa.T).all() and (da == da.T).all())
+        sym = bool((fa == fa.T).all() and (da == da.T).all())
+        self.symmetric = sym and code == _lib.U16          # 2-opt kernels' symmetric sweep
+        self.symmetric_int = sym and code != _lib.F64      # incremental goal halving
         # byte-sized entries with int32-safe sums: the 2-opt dp4a kernel
         mf, md = (int(fa.max()), int(da.max())) if fa.size else (0, 0)
         self.twoopt_bytes = bool(code == _lib.U16 and max(mf, md) < 256 and state.n * mf * md < 2**31)
@@ -563,6 +565,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
     if state.cost_current and state.integral:
         hints |= _lib.HINT_COST_CURRENT
+        if rt.symmetric_int:
+            hints |= _lib.HINT_SYMMETRIC
     rt.coeffs.hints = hints
     passes = config.two_opt_passes
     if passes and not state.integral:
