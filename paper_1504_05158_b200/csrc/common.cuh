@@ -76,7 +76,8 @@ struct DrawRow {
   uint64_t cached;     // block index held in blk (UINT64_MAX = none)
   PhiloxBlock blk;
 
-  __device__ __forceinline__ double at(int k) {
+  // out of line: several call sites (tie draws) in the step kernel
+  __device__ __noinline__ double at(int k) {
     if (inj) return inj[k];
     const uint64_t idx = base + (uint64_t)k;
     const uint64_t b = idx >> 2;
