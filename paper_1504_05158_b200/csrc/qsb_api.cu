@@ -181,9 +181,70 @@ static int launch_twoopt_dp4a(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
+// tensor-core kernel (symmetric, entries < 256, n <= 256): H = [F|P][P|F]^T
+// as one u8 GEMM per pass (twoopt.cuh).  TMEM columns bound the CTAs per SM
+// (a CTA that cannot allocate would spin), so the launch raises its shared
+// memory request until at most 512 / tcols CTAs fit on an SM.
+template <int NT>
+static int launch_twoopt_tc(TwoOptArgs t, cudaStream_t s) {
+  TwoOptTc g{};
+  g.kb = (t.n + 31) / 32 * 32;
+  g.npad = (t.n + 15) / 16 * 16;
+  g.tiles = (t.n + 127) / 128;
+  const int need = g.tiles * g.npad;
+  g.tcols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+  if (g.tiles > 2 || (g.tiles == 2 && NT != 256)) return QSB_EUNSUPPORTED;
+  auto fn = twoopt_tc_kernel<NT>;
+  static size_t dyn_max = 0;
+  if (!dyn_max) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_status(e);
+    dyn_max = smem_optin() - fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  size_t smem = TwoOptTc::smem_bytes(t.n, g.kb, g.tiles, NT);
+  if (smem > dyn_max) return QSB_EUNSUPPORTED;
+  // CTAs per SM from registers, shared memory and TMEM columns (the occupancy
+  // API reports 1 for this kernel, so the limits are applied directly)
+  static int regs = 0, stat = 0;
+  if (!regs) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_status(e);
+    regs = fa.numRegs; stat = (int)fa.sharedSizeBytes;
+  }
+  const int warp_regs = (regs * 32 + 255) / 256 * 256;
+  const int by_regs = 65536 / (warp_regs * (NT / 32));
+  const int by_smem = (int)((smem_optin() + 1024) / (smem + stat + 1024));
+  int bps = by_regs < by_smem ? by_regs : by_smem;
+  if (bps > 512 / g.tcols) bps = 512 / g.tcols;
+  if (getenv("QSB_DEBUG")) fprintf(stderr, "twoopt_tc n=%d smem=%zu bps=%d (regs %d smem %d)\n", t.n, smem, bps, by_regs, by_smem);
+  if (bps < 1) bps = 1;
+  const int64_t cap = (int64_t)num_sms() * bps;
+  const int grid = (int)(t.P < cap ? t.P : cap);
+  if (grid <= 0) return QSB_OK;
+  fn<<<grid, NT, smem, s>>>(t, g);
+  return launch_status();
+}
+
+static bool twoopt_use_dp4a() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QSB_TWOOPT_KERNEL");
+    v = (e && strcmp(e, "dp4a") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <typename MT>
 static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = false) {
   if constexpr (sizeof(MT) == 2) {
+    if (bytes && t.sym && t.n <= 256 && !twoopt_use_dp4a()) {
+      const int rc = t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
+      if (rc != QSB_EUNSUPPORTED) return rc;
+    }
     if (bytes && t.sym) {
       const int rc = t.n <= 32 ? launch_twoopt_dp4a<64>(t, s)
                    : t.n <= 64 ? launch_twoopt_dp4a<128>(t, s)

@@ -356,4 +356,308 @@ __global__ void __launch_bounds__(NT) twoopt_dp4a_kernel(const TwoOptArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-opt on the 5th-generation tensor cores (symmetric instances, byte
+// entries).  The O(n^3) part of a pass is H[r][s] = G[r][s] + G[s][r] of the
+// dp4a kernel above, and H is one GEMM:
+//   H = F P^T + P F^T = [F | P] [P | F]^T        (K = 2n),
+// unsigned 8-bit operands with exact s32 accumulation (tcgen05.mma
+// kind::i8; every H entry is < 2 n 255^2 < 2^32 and non-negative, read as
+// uint32).  F and P sit in shared memory in the canonical K-major,
+// no-swizzle UMMA layout (8-row x 16-byte core matrices); H lands in tensor
+// memory, one TMEM lane per row r, and the epilogue threads read their row
+// with tcgen05.ld and score the swaps (r, s > r) exactly as the dp4a kernel
+// (same int64 delta, same lexicographic (delta, q) order), so the two
+// kernels are interchangeable bit for bit.
+//
+// One CTA per particle at a time; one thread issues the MMAs of a pass
+// (M = 128 rows per tile, 1 or 2 tiles; N = n rounded up to 16; K in steps
+// of 32 bytes) and commits them to an mbarrier the CTA waits on.
+
+// byte offset of (row r, byte k) in the canonical layout with kb bytes per row
+__device__ __forceinline__ int cl_off(int r, int k, int kb) {
+  return (r >> 3) * (kb << 3) + ((k >> 4) << 7) + ((r & 7) << 4) + (k & 15);
+}
+
+// shared-memory matrix descriptor: K-major, no swizzle (layout type 0),
+// LBO = byte distance of K-adjacent core matrices, SBO = of 8-row groups
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ULL << 46);   // descriptor version 1 (sm_100)
+}
+
+// instruction descriptor: u8 x u8 -> s32, both K-major, M x N
+__host__ __device__ constexpr uint32_t umma_idesc_u8(int M, int N) {
+  return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+      :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 16 consecutive 32-bit TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TwoOptTc {
+  int kb;       // bytes per operand row: n rounded up to 32
+  int npad;     // N: n rounded up to 16
+  int tiles;    // M tiles of 128 rows
+  int tcols;    // allocated TMEM columns (power of two >= 32)
+  static __host__ __device__ size_t smem_bytes(int n, int kb, int tiles, int NT) {
+    const size_t mb = (size_t)tiles * 128 * kb;
+    return 2 * mb + align_up((size_t)n * n, 16) + align_up((size_t)n * 4, 16) + (size_t)n * 16 +
+           (NT / 32) * 12 + 64;
+  }
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const TwoOptTc g) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  const int n = a.n, kb = g.kb, npad = g.npad, tiles = g.tiles;
+  const size_t mb = (size_t)tiles * 128 * kb;
+  uint8_t* F8 = tsm;                      // canonical layout, rows >= n and bytes >= n zero
+  uint8_t* P8 = F8 + mb;                  // P = D[p][p], same layout
+  uint8_t* D8 = P8 + mb;                  // D row-major (gather source)
+  int* sp = reinterpret_cast<int*>(D8 + align_up((size_t)n * n, 16));
+  int4* sv = reinterpret_cast<int4*>(sp + align_up((size_t)n, 4));   // per row: {G[r][r], F_rr, P_rr, 0}
+  int64_t* rd = reinterpret_cast<int64_t*>(sv + n);
+  int* rq = reinterpret_cast<int*>(rd + NT / 32);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_move;
+  __shared__ unsigned s_mx[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
+  const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
+
+  if (tid < 2) s_mx[tid] = 0;
+  {
+    uint4* z = reinterpret_cast<uint4*>(F8);
+    const int nz = (int)(2 * mb / 16);
+    for (int i = tid; i < nz; i += NT) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  unsigned mf = 0, md = 0;
+  for (int e = tid; e < n * n; e += NT) {
+    const int r = e / n, c = e - r * n;
+    F8[cl_off(r, c, kb)] = (uint8_t)gF[e];
+    D8[e] = (uint8_t)gD[e];
+    mf = max(mf, (unsigned)gF[e]);
+    md = max(md, (unsigned)gD[e]);
+  }
+  atomicMax(&s_mx[0], mf);
+  atomicMax(&s_mx[1], md);
+  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&s_tmem)), "r"(g.tcols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t idesc = umma_idesc_u8(128, npad);
+  const uint32_t sbo = (uint32_t)kb * 8;
+  const int ksteps = kb / 32;
+  uint32_t phase = 0;
+
+  // epilogue role of this warp: tile t, lane quarter q, column chunks c = h, h + cs, ...
+  const int q = warp & 3;
+  const int t = (NT == 256 && tiles == 2) ? (warp >> 2) : 0;
+  const int h = (NT == 256 && tiles == 1) ? (warp >> 2) : 0;
+  const int cs = (NT == 256 && tiles == 1) ? 2 : 1;
+  const int rbase = t * 128 + q * 32;
+  const int r = rbase + lane;
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * npad);
+  const int nchunks = npad / 16;
+  // n max(F) max(D) < 2^28: every H, G[r][r] and delta fits int32
+  const bool narrow = (double)n * (double)s_mx[0] * (double)s_mx[1] < 268435456.0;
+
+  for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) sp[i] = a.perm[p * n + i];
+    __syncthreads();
+    {
+      // P = D[p][p], 16 bytes per store: a thread keeps one 16-column chunk
+      // (its sp entries in registers) and walks rows; bytes >= n stay zero
+      const int nck = kb >> 4;
+      const int c = tid % nck;
+      int spc[16];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) spc[b] = c * 16 + b < n ? sp[c * 16 + b] : -1;
+      for (int i = tid / nck; i < n; i += NT / nck) {
+        const uint8_t* drow = D8 + sp[i] * n;
+        unsigned w[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          unsigned v = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int j = spc[4 * x + b];
+            v |= (j >= 0 ? (unsigned)drow[j] : 0u) << (8 * b);
+          }
+          w[x] = v;
+        }
+        *reinterpret_cast<uint4*>(P8 + cl_off(i, c * 16, kb)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    uint64_t cost = (uint64_t)a.cost[p];
+    for (int pass = 0; pass < a.passes; ++pass) {
+      __syncthreads();
+      // G[r][r] (4-way byte dot products over the row's 16-byte chunks)
+      for (int rr = tid; rr < n; rr += NT) {
+        unsigned acc = 0;
+        for (int c = 0; c < kb; c += 16) {
+          const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(rr, c, kb));
+          const uint4 d = *reinterpret_cast<const uint4*>(P8 + cl_off(rr, c, kb));
+          acc = __dp4a(f.x, d.x, acc); acc = __dp4a(f.y, d.y, acc);
+          acc = __dp4a(f.z, d.z, acc); acc = __dp4a(f.w, d.w, acc);
+        }
+        sv[rr] = make_int4((int)acc, F8[cl_off(rr, rr, kb)], P8[cl_off(rr, rr, kb)], 0);
+      }
+      fence_proxy_async_smem();   // P8 (generic writes) -> tensor-core reads
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t fa = smem_u32(F8), pa = smem_u32(P8);
+        for (int tt = 0; tt < tiles; ++tt) {
+          const uint32_t aoff = (uint32_t)(tt * 16) * sbo;   // 128 rows = 16 row groups
+          for (int j = 0; j < 2 * ksteps; ++j) {
+            const bool lo = j < ksteps;
+            const uint32_t ko = (uint32_t)(lo ? j : j - ksteps) * 256;
+            const uint64_t ad = umma_smem_desc((lo ? fa : pa) + aoff + ko, 128, sbo);
+            const uint64_t bd = umma_smem_desc((lo ? pa : fa) + ko, 128, sbo);
+            umma_i8(tmem + (uint32_t)(tt * npad), ad, bd, idesc, j > 0 ? 1u : 0u);
+          }
+        }
+        umma_commit(&bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      tc_fence_after();
+
+      // (delta, q) as one ordered key: delta << 32 | q (q >= 0), minimum wins
+      int64_t bkey = INT64_MAX, wbest = INT64_MAX;
+      int wq = INT_MAX;
+      if (rbase < n) {
+        const int4 mine = r < n ? sv[r] : make_int4(0, 0, 0, 0);
+        const int gdr = mine.x, Frr = mine.y, Prr = mine.z;
+        const int qr = r * n - r * (r + 1) / 2 - r - 1;   // q = qr + s
+        for (int c = h; c < nchunks; c += cs) {
+          if (c * 16 + 15 <= rbase) continue;   // whole chunk on or below the diagonal (warp-uniform)
+          uint32_t v[16];
+          tmem_ld16(trow + (uint32_t)(c * 16), v);
+          if (r >= n) continue;
+          const uint4 fr = *reinterpret_cast<const uint4*>(F8 + cl_off(r, c * 16, kb));
+          const uint4 pr = *reinterpret_cast<const uint4*>(P8 + cl_off(r, c * 16, kb));
+          const unsigned fw[4] = {fr.x, fr.y, fr.z, fr.w};
+          const unsigned pw[4] = {pr.x, pr.y, pr.z, pr.w};
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int s = c * 16 + j;
+            if (s <= r || s >= n) continue;
+            const int4 o = sv[s];
+            const int Frs = (fw[j >> 2] >> (8 * (j & 3))) & 0xff;
+            const int Prs = (pw[j >> 2] >> (8 * (j & 3))) & 0xff;
+            // cross terms and the diagonal product are < 2^17 in magnitude
+            const int x = (Frr - Frs) * (Prs - Prr) + (Frs - o.y) * (o.z - Prs);
+            const int y = (Frr - o.y) * (o.z - Prr);
+            if (narrow) {
+              // (delta, q) as one ordered key, delta << 32 | q (q >= 0)
+              const int dd = y + 2 * ((int)v[j] - gdr - o.x - x);
+              const int64_t key = (int64_t)((uint64_t)(int64_t)dd << 32) | (int64_t)(qr + s);
+              bkey = key < bkey ? key : bkey;
+            } else {
+              const int64_t dd = (int64_t)y + 2 * ((int64_t)v[j] - gdr - o.x - x);
+              if (dd < wbest || (dd == wbest && qr + s < wq)) { wbest = dd; wq = qr + s; }
+            }
+          }
+        }
+      }
+      // narrow: delta = key >> 32 (arithmetic), q = low word; INT64_MAX = none
+      int64_t best = wbest;
+      int bq = wq;
+      if (narrow && bkey != INT64_MAX) { best = bkey >> 32; bq = (int)(bkey & 0xffffffff); }
+      tc_fence_before();
+      // lexicographic (delta, q) minimum over the CTA
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      if (lane == 0) { rd[warp] = best; rq[warp] = bq; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < NT / 32; ++w)
+          if (rd[w] < rd[0] || (rd[w] == rd[0] && rq[w] < rq[0])) { rd[0] = rd[w]; rq[0] = rq[w]; }
+        s_move = (rq[0] != INT_MAX && rd[0] < 0) ? rq[0] : -1;
+      }
+      __syncthreads();
+      const int mq = s_move;
+      if (mq < 0) break;
+      cost += (uint64_t)rd[0];
+      int r0, s0;
+      unrank_pair(mq, n, r0, s0);
+      // swap facilities r0 and s0: rows, then columns of P
+      for (int j = tid; j < n; j += NT) {
+        const int ir = cl_off(r0, j, kb), is = cl_off(s0, j, kb);
+        const uint8_t x = P8[ir]; P8[ir] = P8[is]; P8[is] = x;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += NT) {
+        const int ir = cl_off(i, r0, kb), is = cl_off(i, s0, kb);
+        const uint8_t x = P8[ir]; P8[ir] = P8[is]; P8[is] = x;
+      }
+      if (tid == 0) { const int x = sp[r0]; sp[r0] = sp[s0]; sp[s0] = x; }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) a.perm[p * n + i] = (int16_t)sp[i];
+    if (a.do_pbest) {
+      if (tid == 0) {
+        const bool imp = (int64_t)cost < a.pl_cost[p];
+        if (imp) a.pl_cost[p] = (int64_t)cost;
+        a.improved[p] = imp ? 1 : 0;
+        s_move = imp;
+      }
+      __syncthreads();
+      if (s_move)
+        for (int i = tid; i < n; i += NT) a.pl_perm[p * n + i] = (int16_t)sp[i];
+    }
+    if (tid == 0) a.cost[p] = (int64_t)cost;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(g.tcols) : "memory");
+  }
+}
+
 }  // namespace qsb

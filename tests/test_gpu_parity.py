@@ -415,8 +415,9 @@ def test_north_star_shape_properties():
 
 
 # ------------------------------------------------------------------ 2-opt
-@pytest.mark.parametrize("n,sym", [(12, True), (30, True), (30, False), (64, False),
-                                   (65, True), (100, False), (200, True)])
+@pytest.mark.parametrize("n,sym", [(2, True), (12, True), (30, True), (30, False), (33, True), (50, True),
+                                   (64, False), (65, True), (100, False), (128, True), (129, True),
+                                   (200, True)])
 @pytest.mark.parametrize("passes", [1, 4])
 def test_twoopt_many_vs_oracle(n, sym, passes):
     rng = np.random.default_rng(n * 10 + passes)
@@ -486,7 +487,7 @@ def test_collect_device_equals_host_collect(precision, instance, golden_instance
         qsb.step(st, inst, cfg)
 
 
-@pytest.mark.parametrize("n", [96, 128, 256])
+@pytest.mark.parametrize("n", [96, 128, 255, 256])
 def test_twoopt_large_symmetric_vs_oracle(n):
     rng = np.random.default_rng(n)
     f = np.triu(rng.integers(0, 100, (n, n)), 1)
