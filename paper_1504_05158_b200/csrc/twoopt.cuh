@@ -429,8 +429,8 @@ struct TwoOptTc {
   int tcols;    // allocated TMEM columns (power of two >= 32)
   static __host__ __device__ size_t smem_bytes(int n, int kb, int tiles, int NT) {
     const size_t mb = (size_t)tiles * 128 * kb;
-    return 2 * mb + align_up((size_t)n * n, 16) + align_up((size_t)n * 4, 16) + (size_t)n * 16 +
-           (NT / 32) * 12 + 64;
+    return 2 * mb + align_up((size_t)n * (n + 1), 16) + align_up((size_t)n * 4, 16) +
+           (size_t)(n + 15) / 16 * 256 + (NT / 32) * 12 + 64;
   }
 };
 
@@ -441,10 +441,11 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
   const size_t mb = (size_t)tiles * 128 * kb;
   uint8_t* F8 = tsm;                      // canonical layout, rows >= n and bytes >= n zero
   uint8_t* P8 = F8 + mb;                  // P = D[p][p], same layout
-  uint8_t* D8 = P8 + mb;                  // D row-major (gather source)
-  int* sp = reinterpret_cast<int*>(D8 + align_up((size_t)n * n, 16));
+  uint8_t* D8 = P8 + mb;                  // D row-major, row stride n + 1, column n zero
+  const int dn = n + 1;
+  int* sp = reinterpret_cast<int*>(D8 + align_up((size_t)n * dn, 16));
   int4* sv = reinterpret_cast<int4*>(sp + align_up((size_t)n, 4));   // per row: {G[r][r], F_rr, P_rr, 0}
-  int64_t* rd = reinterpret_cast<int64_t*>(sv + n);
+  int64_t* rd = reinterpret_cast<int64_t*>(sv + (n + 15) / 16 * 16);
   int* rq = reinterpret_cast<int*>(rd + NT / 32);
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t s_tmem;
@@ -465,10 +466,11 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
   for (int e = tid; e < n * n; e += NT) {
     const int r = e / n, c = e - r * n;
     F8[cl_off(r, c, kb)] = (uint8_t)gF[e];
-    D8[e] = (uint8_t)gD[e];
+    D8[r * dn + c] = (uint8_t)gD[e];
     mf = max(mf, (unsigned)gF[e]);
     md = max(md, (unsigned)gD[e]);
   }
+  for (int r = tid; r < n; r += NT) D8[r * dn + n] = 0;
   atomicMax(&s_mx[0], mf);
   atomicMax(&s_mx[1], md);
   if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
@@ -509,19 +511,15 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
       const int c = tid % nck;
       int spc[16];
 #pragma unroll
-      for (int b = 0; b < 16; ++b) spc[b] = c * 16 + b < n ? sp[c * 16 + b] : -1;
+      for (int b = 0; b < 16; ++b) spc[b] = c * 16 + b < n ? sp[c * 16 + b] : n;   // n: the zero column
       for (int i = tid / nck; i < n; i += NT / nck) {
-        const uint8_t* drow = D8 + sp[i] * n;
+        const uint8_t* drow = D8 + sp[i] * dn;
         unsigned w[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          unsigned v = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int j = spc[4 * x + b];
-            v |= (j >= 0 ? (unsigned)drow[j] : 0u) << (8 * b);
-          }
-          w[x] = v;
+          const unsigned b0 = drow[spc[4 * x]], b1 = drow[spc[4 * x + 1]];
+          const unsigned b2 = drow[spc[4 * x + 2]], b3 = drow[spc[4 * x + 3]];
+          w[x] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
         }
         *reinterpret_cast<uint4*>(P8 + cl_off(i, c * 16, kb)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
@@ -562,13 +560,14 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
       phase ^= 1u;
       tc_fence_after();
 
-      // (delta, q) as one ordered key: delta << 32 | q (q >= 0), minimum wins
-      int64_t bkey = INT64_MAX, wbest = INT64_MAX;
-      int wq = INT_MAX;
+      // delta(r, s) = 2 (H - G_rr - G_ss) + (2 F_rs - F_rr - F_ss)(2 P_rs - P_rr - P_ss),
+      // the dp4a kernel's delta regrouped; a thread walks s upwards, so a
+      // strict < keeps the first q of its row
+      int bd = INT_MAX, bs = -1;                 // narrow: int32 deltas
+      int64_t wbd = INT64_MAX;
       if (rbase < n) {
         const int4 mine = r < n ? sv[r] : make_int4(0, 0, 0, 0);
         const int gdr = mine.x, Frr = mine.y, Prr = mine.z;
-        const int qr = r * n - r * (r + 1) / 2 - r - 1;   // q = qr + s
         for (int c = h; c < nchunks; c += cs) {
           if (c * 16 + 15 <= rbase) continue;   // whole chunk on or below the diagonal (warp-uniform)
           uint32_t v[16];
@@ -581,29 +580,25 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int s = c * 16 + j;
-            if (s <= r || s >= n) continue;
             const int4 o = sv[s];
-            const int Frs = (fw[j >> 2] >> (8 * (j & 3))) & 0xff;
-            const int Prs = (pw[j >> 2] >> (8 * (j & 3))) & 0xff;
-            // cross terms and the diagonal product are < 2^17 in magnitude
-            const int x = (Frr - Frs) * (Prs - Prr) + (Frs - o.y) * (o.z - Prs);
-            const int y = (Frr - o.y) * (o.z - Prr);
+            const int Frs = (int)__byte_perm(fw[j >> 2], 0u, 0x4440 | (j & 3));
+            const int Prs = (int)__byte_perm(pw[j >> 2], 0u, 0x4440 | (j & 3));
+            const int t = (2 * Frs - Frr - o.y) * (2 * Prs - Prr - o.z);   // |t| < 2^18
+            const bool ok = s > r && s < n;
             if (narrow) {
-              // (delta, q) as one ordered key, delta << 32 | q (q >= 0)
-              const int dd = y + 2 * ((int)v[j] - gdr - o.x - x);
-              const int64_t key = (int64_t)((uint64_t)(int64_t)dd << 32) | (int64_t)(qr + s);
-              bkey = key < bkey ? key : bkey;
+              // n max(F) max(D) < 2^28: H, G and the delta fit int32
+              const int dd = 2 * ((int)v[j] - gdr - o.x) + t;
+              if (ok && dd < bd) { bd = dd; bs = s; }
             } else {
-              const int64_t dd = (int64_t)y + 2 * ((int64_t)v[j] - gdr - o.x - x);
-              if (dd < wbest || (dd == wbest && qr + s < wq)) { wbest = dd; wq = qr + s; }
+              const int64_t dd = 2 * ((int64_t)v[j] - gdr - o.x) + t;
+              if (ok && dd < wbd) { wbd = dd; bs = s; }
             }
           }
         }
       }
-      // narrow: delta = key >> 32 (arithmetic), q = low word; INT64_MAX = none
-      int64_t best = wbest;
-      int bq = wq;
-      if (narrow && bkey != INT64_MAX) { best = bkey >> 32; bq = (int)(bkey & 0xffffffff); }
+      const int qr = r * n - r * (r + 1) / 2 - r - 1;   // q = qr + s
+      int64_t best = bs < 0 ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
+      int bq = bs < 0 ? INT_MAX : qr + bs;
       tc_fence_before();
       // lexicographic (delta, q) minimum over the CTA
 #pragma unroll
