@@ -706,7 +706,29 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
       }
       return;
     }
+    // batches of 8 rows, loads first (latency-bound walk for GT tiles);
+    // even rows feed the first chain, odd rows the second, as below
+    constexpr int RB = 8;
     int r = 0;
+    for (; r + RB <= n; r += RB) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        VT* cell = tile + r * n + col[k];
+        VT x[RB];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) x[b] = cell[b * n];
+        if constexpr (decltype(do_scale)::value) {
+#pragma unroll
+          for (int b = 0; b < RB; ++b) { x[b] = rescale(x[b], k); cell[b * n] = x[b]; }
+        }
+#pragma unroll
+        for (int b = 0; b < RB; b += 2) {
+          upd(x[b], r + b, k, nmax[k], ncnt[k], nrow[k]);
+          upd(x[b + 1], r + b + 1, k, mB[k], cB[k], rB[k]);
+        }
+      }
+    }
     for (; r + 1 < n; r += 2) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
@@ -841,7 +863,26 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
     if (v_bounded) run(std::false_type{});
     else run(std::true_type{});
   } else {
+    // batches of 8 rows, loads first: with the tile in global memory (GT)
+    // the column walk is latency-bound unless many loads are in flight
+    constexpr int RB = 8;
     int r = 0;
+    for (; r + RB <= n; r += RB) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
+        float x[RB];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) x[b] = cell[b * n];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          const float l = fminf(fmaxf(c1k[k] * x[b], -vmc), vmc);
+          cell[b * n] = l;
+          if (b & 1) tot2[k] += fabsf(l); else tot[k] += fabsf(l);
+        }
+      }
+    }
     for (; r + 1 < n; r += 2) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
@@ -1148,13 +1189,28 @@ step_kernel(const StepArgs a) {
         double tot[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) tot[k] = 0.0;
+        // loads issued 8 rows ahead (GT tiles live in global memory); the
+        // arithmetic and the column sum stay in row order
+        constexpr int RB = 8;
+        double xb[CPL][RB];
         for (int r = 0; r < n; ++r) {
+          if ((r & (RB - 1)) == 0) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              if (!cfree[k]) continue;
+#pragma unroll
+              for (int b = 0; b < RB; ++b)
+                if (r + b < n) xb[k][b] = tile[(r + b) * n + col[k]];
+            }
+          }
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
             if (!cfree[k]) continue;
             const int xr = zr[k], lr = plr[k], gr = pgr[k];
             double* cell = tile + r * n + col[k];
-            const double v = *cell;
+            double v = xb[k][0];
+#pragma unroll
+            for (int b = 1; b < RB; ++b) if ((r & (RB - 1)) == b) v = xb[k][b];
             const bool special = r == xr || r == lr || r == gr;
             double lin;
             if (special) {
@@ -1349,8 +1405,24 @@ step_kernel(const StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) { nmax[k] = so.m[k]; ncnt[k] = so.c[k]; nrow[k] = so.r[k]; }
     } else if (!lazy) {
+      // normalisation only (no aggregation): batches of 8 rows, loads first
+      constexpr int RB = 8;
+      int r = 0;
 #pragma unroll 1
-      for (int r = 0; r < n; ++r) {
+      for (; r + RB <= n; r += RB) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          if (!scale[k]) continue;
+          VT* cell = tile + r * n + col[k];
+          VT x[RB];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) x[b] = cell[b * n];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) cell[b * n] = rescale(x[b], k);
+        }
+      }
+#pragma unroll 1
+      for (; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
           if (scale[k]) tile[r * n + col[k]] = rescale(tile[r * n + col[k]], k);
