@@ -401,7 +401,9 @@ __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vst
       if (e < nn) {
         const uint64_t idx = base + (uint64_t)e;
         const double u = u64_to_unit(philox4x64_10((idx >> 2) + 1, seed, word1).v[idx & 3]);
-        vp[e] = (VT)(-amp + 2.0 * amp * u);
+        const double v = -amp + 2.0 * amp * u;
+        if constexpr (sizeof(VT) == 4) vp[e] = n <= WIDE_MAX_N ? (VT)wenc(v) : (VT)v;
+        else vp[e] = (VT)v;
       } else {
         vp[e] = (VT)0;
       }

@@ -117,6 +117,17 @@ __device__ __forceinline__ double cell_m(VT v, bool x_one) {
   return __dadd_rn(x_one ? 1.0 : 0.0, (double)v);
 }
 
+// ------------------------------------------------ wide 32-bit velocity words
+// fp32 velocity tiles with n <= 64 (the one-warp step kernels) store the high
+// word of the double (sign, 11-bit exponent, 20-bit fraction), rounded to
+// nearest: fp32's size with fp64's exponent range (step_kernel.cuh, vval).
+constexpr int WIDE_MAX_N = 64;
+__device__ __forceinline__ double wdec(float w) { return __hiloint2double(__float_as_int(w), 0); }
+__device__ __forceinline__ float wenc(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d) + 0x80000000ULL;
+  return __int_as_float((int)(unsigned)(b >> 32));
+}
+
 // -------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -258,21 +258,43 @@ __device__ __forceinline__ int group_min_int(int x, Scratch& sc, int& ipar, int 
   return x;
 }
 
-// Velocity value of a stored entry.  fp64 tiles hold v itself; fp32 tiles
-// hold u with v = u * s (s the column scale of the lazily scaled layout, 1.0
-// otherwise), and the product is exact in double.
-template <typename VT>
+// Velocity value of a stored entry.  fp64 tiles hold v itself.  fp32 tiles
+// of the one-warp kernels (G == 1) hold "wide" 32-bit words: the high word
+// of the double (sign, 11-bit exponent, 20-bit fraction), rounded to
+// nearest -- the byte size of fp32 with the exponent range of fp64, so an
+// entry the reference keeps as a tiny non-zero value (it decays by ~1 bit
+// per step while x / pl / pg leave it alone) does not flush to zero after
+// ~150 steps as an fp32 would, and does not turn into a spurious tie.  The
+// words order like floats (sign-magnitude), so stored values are compared
+// with float compares on the raw bits (exact for |v| in [2^-1015, 2^1017];
+// no flush-to-zero in this build).  Multi-warp fp32 tiles hold plain
+// floats.  Lazily scaled: v = u * s (s the column scale, 1.0 otherwise);
+// the product is exact in double.
+template <typename VT, int G>
+struct Wide { static constexpr bool value = sizeof(VT) == 4 && G == 1; };
+
+template <typename VT, int G>
+__device__ __forceinline__ double vdec(VT u) {   // stored word -> value (unscaled)
+  if constexpr (Wide<VT, G>::value) return wdec(u);
+  else return (double)u;
+}
+template <typename VT, int G>
+__device__ __forceinline__ VT venc(double v) {   // value -> stored word
+  if constexpr (Wide<VT, G>::value) return wenc(v);
+  else return (VT)v;
+}
+template <typename VT, int G>
 __device__ __forceinline__ double vval(VT u, float s) {
   if constexpr (sizeof(VT) == 8) return u;
-  else return (double)u * (double)s;
+  else return vdec<VT, G>(u) * (double)s;
 }
-template <typename VT>
+template <typename VT, int G>
 __device__ __forceinline__ uint64_t nonz_key(VT v, float s) {   // key of m = 0.0 + v
-  return okey(__dadd_rn(0.0, vval(v, s)));
+  return okey(__dadd_rn(0.0, vval<VT, G>(v, s)));
 }
-template <typename VT>
+template <typename VT, int G>
 __device__ __forceinline__ uint64_t z_key(VT v, float s) {      // key of m = 1.0 + v
-  return okey(__dadd_rn(1.0, vval(v, s)));
+  return okey(__dadd_rn(1.0, vval<VT, G>(v, s)));
 }
 
 // Set of free rows (bit r of word r/64).
@@ -288,9 +310,9 @@ struct RowSet {
   }
 };
 
-template <typename VT>
+template <typename VT, int G>
 __device__ __forceinline__ uint64_t mkey(const VT* tile, const float* sS, int n, int r, int c, int zrc) {
-  return okey(__dadd_rn(r == zrc ? 1.0 : 0.0, vval(tile[r * n + c], sS[c])));
+  return okey(__dadd_rn(r == zrc ? 1.0 : 0.0, vval<VT, G>(tile[r * n + c], sS[c])));
 }
 
 // ---- rare paths, kept out of line so the round loop stays in I-cache ----
@@ -326,7 +348,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
         if (!tf) continue;
         const int zc = sc.szr[c];
         if (r == zc && tf != 2) continue;
-        if (mkey(tile, sc.sS, n, r, c, zc) == key) ++cnt;
+        if (mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) ++cnt;
       }
     }
     sc.srow[r] = cnt;
@@ -341,7 +363,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
       if (!tf) continue;
       const int zc = sc.szr[c];
       if (r == zc && tf != 2) continue;
-      if (mkey(tile, sc.sS, n, r, c, zc) == key) {
+      if (mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) {
         if (q == 0) { cc = c; break; }
         --q;
       }
@@ -360,7 +382,7 @@ __device__ __noinline__ int first_row_scan(const VT* tile, int n, Scratch& sc, R
   const int zc = sc.szr[c];
   int found = INT_MAX;
   for (int r = tid; r < n; r += NT)
-    if (rf.has(r) && (r != zc || zok) && mkey(tile, sc.sS, n, r, c, zc) == key) found = min(found, r);
+    if (rf.has(r) && (r != zc || zok) && mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) found = min(found, r);
   return group_min_sync<G>(found, sc, lane, tid);
 }
 
@@ -433,8 +455,8 @@ __device__ __noinline__ int tie_select_warp(const VT* tile, int n, Scratch& sc, 
       b &= b - 1;
       const int zc = sc.szr[c];
       const bool zok = sc.stie[c] == 2;
-      const bool a0 = r0ok && (c0 != zc || zok) && mkey(tile, sc.sS, n, c0, c, zc) == key;
-      const bool a1 = r1ok && (c1 != zc || zok) && mkey(tile, sc.sS, n, c1, c, zc) == key;
+      const bool a0 = r0ok && (c0 != zc || zok) && mkey<VT, 1>(tile, sc.sS, n, c0, c, zc) == key;
+      const bool a1 = r1ok && (c1 != zc || zok) && mkey<VT, 1>(tile, sc.sS, n, c1, c, zc) == key;
       const unsigned m0 = __ballot_sync(FULL, a0), m1 = __ballot_sync(FULL, a1);
       cnt0 += a0;
       cnt1 += a1;
@@ -495,7 +517,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
     Best rb = best_none();
     for (int r = tid; r < n; r += NT) {
       if (!rf.has(r)) continue;
-      const uint64_t key = mkey(tile, sc.sS, n, r, c, zc);
+      const uint64_t key = mkey<VT, G>(tile, sc.sS, n, r, c, zc);
       if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
       else if (key == rb.key) ++rb.cnt;
     }
@@ -506,7 +528,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
       const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
       const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
       for (int r = tid; r < n; r += NT)
-        sc.srow[r] = (rf.has(r) && mkey(tile, sc.sS, n, r, c, zc) == b.key) ? 1 : 0;
+        sc.srow[r] = (rf.has(r) && mkey<VT, G>(tile, sc.sS, n, r, c, zc) == b.key) ? 1 : 0;
       GroupSync<G>::sync();
       if (tid == 0) {
         int q = pick, r = 0;
@@ -586,7 +608,7 @@ struct ColOut {
   int c[CPL], r[CPL];
 };
 
-template <typename VT, int CPL>
+template <typename VT, int G, int CPL>
 __device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const ColIn<VT, CPL> in) {
   const VT NINF = (VT)(-INFINITY);
   ColOut<VT, CPL> o;
@@ -600,6 +622,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const Col
       VT v = *cell;
       if (in.scale[k]) {
         if constexpr (sizeof(VT) == 8) v = __ddiv_rn(v, in.total[k]);
+        else if constexpr (Wide<VT, G>::value) v = wenc(wdec(v) * (double)in.inv[k]);
         else v = v * in.inv[k];
         *cell = v;
       }
@@ -632,6 +655,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
   }
   auto rescale = [&](VT v, int k) -> VT {
     if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
+    else if constexpr (Wide<VT, G>::value) return wenc(wdec(v) * (double)inv[k]);
     else return v * inv[k];
   };
   // Max / tie count / first row over the non-z rows (the z row is masked
@@ -670,7 +694,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
       const int n2 = 2 * n;
       auto sc_ = [&](VT v, VT f, int k) -> VT {
         if constexpr (sizeof(VT) == 8) return k == 0 || live1 ? __ddiv_rn(v, total[k]) : v;
-        else return v * f;
+        else return wenc(wdec(v) * (double)f);   // G == 1 here: wide words
       };
       auto upd2 = [&](VT w, int r, int, VT& m, int& c, int& rr) {
         const bool gt = w > m;
@@ -759,7 +783,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
   } else if (smode == 1) {
     stats_rows(std::true_type{});   // the normalised (norm mode) path
   } else {
-    const ColOut<VT, CPL> g = stats_generic<VT, CPL>(tile, n, in);
+    const ColOut<VT, CPL> g = stats_generic<VT, G, CPL>(tile, n, in);
 #pragma unroll
     for (int k = 0; k < CPL; ++k) { nmax[k] = g.m[k]; ncnt[k] = g.c[k]; nrow[k] = g.r[k]; }
   }
@@ -793,6 +817,9 @@ struct VelOut { float total[CPL]; };
 template <int G, int CPL>
 __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn<CPL> in, double c1,
                                                  double c2r2, double c3r3, double vmax, int v_bounded) {
+  // G == 1: the tile holds wide words (see wdec / wenc), decoded to double,
+  // scaled and clamped in double, re-encoded; G > 1: plain floats
+  constexpr bool WF = G == 1;
   VelOut<CPL> o;
   int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
   bool cfree[CPL];
@@ -809,8 +836,9 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   const float c1f = (float)c1;
   const float vm = (float)vmax;
   float c1k[CPL];
+  double c1kd[CPL];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) c1k[k] = c1f * cs[k];
+  for (int k = 0; k < CPL; ++k) { c1k[k] = c1f * cs[k]; c1kd[k] = (double)c1f * (double)cs[k]; }
   float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
@@ -829,6 +857,20 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   for (int k = 0; k < CPL; ++k) tot2[k] = 0.f;
   // |c1 v| <= v_max guaranteed for every stored v: the clamp is a no-op
   const float vmc = v_bounded ? __int_as_float(0x7f800000) : vm;
+  const double vmcd = v_bounded ? (double)__int_as_float(0x7f800000) : vmax;
+  // one stored word scaled by the column factor and clamped; returns the
+  // word to store, and the value's magnitude for the column sum
+  auto step1 = [&](float w, int k, float f, double fd, float& mag) -> float {
+    if constexpr (WF) {
+      const double x = fmin(fmax(fd * wdec(w), -vmcd), vmcd);
+      mag = (float)fabs(x);
+      return wenc(x);
+    } else {
+      const float x = fminf(fmaxf(f * w, -vmc), vmc);
+      mag = fabsf(x);
+      return x;
+    }
+  };
   if constexpr (G == 1 && CPL == 2) {
     // n in 33..64: slot 0 is live in every lane; a dead slot 1 re-runs
     // slot 0's column with a unit factor (same thread, idempotent),
@@ -836,28 +878,28 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
     const bool live1 = cfree[1];
     float* q0 = reinterpret_cast<float*>(tile) + col[0];
     float* q1 = reinterpret_cast<float*>(tile) + (live1 ? col[1] : col[0]);
-    const float f0 = c1k[0];
-    const float f1 = live1 ? c1k[1] : 1.0f;
+    const double f0 = c1kd[0];
+    const double f1 = live1 ? c1kd[1] : 1.0;
     const int n2 = 2 * n;
     auto run = [&](auto clampit) {
-      auto cl = [&](float x) -> float {
-        if constexpr (decltype(clampit)::value) return fminf(fmaxf(x, -vmc), vmc);
+      auto cl = [&](double x) -> double {
+        if constexpr (decltype(clampit)::value) return fmin(fmax(x, -vmcd), vmcd);
         else return x;
       };
       int r = 0;
       for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
-        const float a0 = cl(f0 * q0[0]), a1 = cl(f0 * q0[n]);
-        q0[0] = a0; q0[n] = a1;
-        tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
-        const float b0 = cl(f1 * q1[0]), b1 = cl(f1 * q1[n]);
-        q1[0] = b0; q1[n] = b1;
-        tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
+        const double a0 = cl(f0 * wdec(q0[0])), a1 = cl(f0 * wdec(q0[n]));
+        q0[0] = wenc(a0); q0[n] = wenc(a1);
+        tot[0] += (float)fabs(a0); tot2[0] += (float)fabs(a1);
+        const double b0 = cl(f1 * wdec(q1[0])), b1 = cl(f1 * wdec(q1[n]));
+        q1[0] = wenc(b0); q1[n] = wenc(b1);
+        tot[1] += (float)fabs(b0); tot2[1] += (float)fabs(b1);
       }
       if (r < n) {
-        const float a0 = cl(f0 * q0[0]);
-        q0[0] = a0; tot[0] += fabsf(a0);
-        const float b0 = cl(f1 * q1[0]);
-        q1[0] = b0; tot[1] += fabsf(b0);
+        const double a0 = cl(f0 * wdec(q0[0]));
+        q0[0] = wenc(a0); tot[0] += (float)fabs(a0);
+        const double b0 = cl(f1 * wdec(q1[0]));
+        q1[0] = wenc(b0); tot[1] += (float)fabs(b0);
       }
     };
     if (v_bounded) run(std::false_type{});
@@ -877,33 +919,20 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
         for (int b = 0; b < RB; ++b) x[b] = cell[b * n];
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
-          const float l = fminf(fmaxf(c1k[k] * x[b], -vmc), vmc);
-          cell[b * n] = l;
-          if (b & 1) tot2[k] += fabsf(l); else tot[k] += fabsf(l);
+          float mag;
+          cell[b * n] = step1(x[b], k, c1k[k], c1kd[k], mag);
+          if (b & 1) tot2[k] += mag; else tot[k] += mag;
         }
       }
     }
-    for (; r + 1 < n; r += 2) {
+    for (; r < n; ++r) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
         float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-        const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
-        const float l1 = fminf(fmaxf(c1k[k] * cell[n], -vmc), vmc);
-        cell[0] = l0;
-        cell[n] = l1;
-        tot[k] += fabsf(l0);
-        tot2[k] += fabsf(l1);
-      }
-    }
-    if (r < n) {
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        if (!cfree[k]) continue;
-        float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
-        const float l0 = fminf(fmaxf(c1k[k] * cell[0], -vmc), vmc);
-        cell[0] = l0;
-        tot[k] += fabsf(l0);
+        float mag;
+        cell[0] = step1(cell[0], k, c1k[k], c1kd[k], mag);
+        tot[k] += mag;
       }
     }
   }
@@ -917,12 +946,21 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
     auto fix = [&](int r, float v0) {
       const float d2 = (float)((r == lr) - (r == xr));
       const float d3 = (float)((r == gr) - (r == xr));
-      const float g = fminf(fmaxf(c1k[k] * v0, -vm), vm);
-      // in double: the pulls and the inertia term can cancel
-      const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * ((double)v0 * (double)cs[k])));
-      const float sp = (float)fmin(fmax(l, -vmax), vmax);
-      colp[r * n] = sp;
-      tot[k] += fabsf(sp) - fabsf(g);
+      // the loop's value for this row (its magnitude is in the sum), then
+      // the exact one; in double: the pulls and the inertia term can cancel
+      float gmag;
+      (void)step1(v0, k, c1k[k], c1kd[k], gmag);
+      const double vd = WF ? wdec(v0) : (double)v0;
+      const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * (vd * (double)cs[k])));
+      if constexpr (WF) {
+        const double sp = fmin(fmax(l, -vmax), vmax);
+        colp[r * n] = wenc(sp);
+        tot[k] += (float)fabs(sp) - gmag;
+      } else {
+        const float sp = (float)fmin(fmax(l, -vmax), vmax);
+        colp[r * n] = sp;
+        tot[k] += fabsf(sp) - gmag;
+      }
     };
     fix(xr, vx[k]);
     if (lr != xr) fix(lr, vl[k]);
@@ -932,10 +970,56 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   return o;
 }
 
+// Loads of particle pp into the group's staging area: one bulk copy of the
+// tile (and, lazily scaled, its column state) on the group's mbarrier, and
+// cp.async copies of the perm / pl_perm / pg_perm rows, (c2 r2, c3 r3) and
+// (cost, pl_cost) into buffer `buf`.  Out of line: it has two call sites
+// (the first particle and the prefetch after the aggregation), and one copy
+// keeps the per-particle path smaller in the instruction cache.
+enum LoadFlags : int { L_LAZY = 1, L_PERM = 2, L_COST = 4, L_PL = 8, L_VEL = 16 };
+
+template <typename K, typename VT>
+__device__ __noinline__ void issue_particle_load(const StepArgs* ap, int64_t pp, int buf, int tid,
+                                                 int lane, VT* tile, unsigned char* stg, uint64_t* bar,
+                                                 uint32_t tile_bytes, uint32_t col_bytes, int lf,
+                                                 double inv_s) {
+  const StepArgs& a = *ap;
+  if (tid == 0) {
+    bulk_wait_read();                 // the previous bulk store has left the tile
+    const bool lz = K::STAGE && (lf & L_LAZY);
+    mbar_arrive_expect_tx(bar, tile_bytes + (lz ? col_bytes : 0u));
+    bulk_load(tile, reinterpret_cast<const VT*>(a.V) + pp * a.vstride, tile_bytes, bar);
+    if (lz) bulk_load(stg + K::SCOL, a.vcol + pp * 5 * (int64_t)a.vcstride, col_bytes, bar);
+  }
+  if constexpr (K::STAGE) {
+    const int n = a.n;
+    int16_t* s_perm = reinterpret_cast<int16_t*>(stg + K::SPERM);
+    if (lf & L_PERM) {
+      const int nw = n >> 1;
+      const int64_t ss = (int64_t)__fma_rn((double)pp, inv_s, 0x1p-26);
+#pragma unroll 1
+      for (int w = lane; w < nw; w += 32) {
+        cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
+        if (lf & L_VEL) {
+          cp_async4(s_perm + K::NMAX + 2 * w, a.pl_perm + pp * n + 2 * w);
+          cp_async4(s_perm + 2 * K::NMAX + 2 * w, a.pg_perm + ss * n + 2 * w);
+        }
+      }
+    }
+    if (lane == 0) {
+      int64_t* s_cost = reinterpret_cast<int64_t*>(stg + K::SCOST);
+      if ((lf & L_VEL) && a.coef) cp_async16(stg + K::SCOEF, a.coef + 2 * pp);
+      if (lf & L_COST) cp_async8(s_cost + 2 * buf, reinterpret_cast<const int64_t*>(a.cost) + pp);
+      if (lf & L_PL) cp_async8(s_cost + 2 * buf + 1, reinterpret_cast<const int64_t*>(a.pl_cost) + pp);
+    }
+    cp_async_commit();
+  }
+}
+
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 __global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : 1))
-step_kernel(const StepArgs a) {
+step_kernel(const __grid_constant__ StepArgs a) {
   // GT: the particle tile stays in global memory (L1/L2-cached) instead of
   // being staged in smem -- used when an n x n tile exceeds shared memory.
   using K = StepKernel<VT, MT, G, CPL, W, GT>;
@@ -1039,32 +1123,11 @@ step_kernel(const StepArgs a) {
   auto swarm_of = [&](int64_t pp) -> int64_t {
     return (int64_t)__fma_rn((double)pp, inv_s, 0x1p-26);
   };
+  const int lflags = (lazy ? L_LAZY : 0) | (stage_perm ? L_PERM : 0) | (stage_cost ? L_COST : 0) |
+                     (stage_pl ? L_PL : 0) | (do_vel ? L_VEL : 0);
   auto issue_load = [&](int64_t pp, int buf) {
-    if (tid == 0) {
-      bulk_wait_read();                 // the previous bulk store has left the tile
-      mbar_arrive_expect_tx(&sc.bar, tile_bytes + (K::STAGE && lazy ? col_bytes : 0u));
-      bulk_load(tile, reinterpret_cast<VT*>(a.V) + pp * a.vstride, tile_bytes, &sc.bar);
-      if (K::STAGE && lazy) bulk_load(s_col, a.vcol + pp * 5 * (int64_t)vcs, col_bytes, &sc.bar);
-    }
-    if constexpr (K::STAGE) {
-      if (stage_perm) {
-        const int nw = n >> 1;
-        const int64_t ss = swarm_of(pp);
-        for (int w = lane; w < nw; w += 32) {
-          cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
-          if (do_vel) {
-            cp_async4(s_perm + K::NMAX + 2 * w, a.pl_perm + pp * n + 2 * w);
-            cp_async4(s_perm + 2 * K::NMAX + 2 * w, a.pg_perm + ss * n + 2 * w);
-          }
-        }
-      }
-      if (lane == 0) {
-        if (do_vel && a.coef) cp_async16(s_coef, a.coef + 2 * pp);
-        if (stage_cost) cp_async8(s_cost + 2 * buf, reinterpret_cast<const int64_t*>(a.cost) + pp);
-        if (stage_pl) cp_async8(s_cost + 2 * buf + 1, reinterpret_cast<const int64_t*>(a.pl_cost) + pp);
-      }
-      cp_async_commit();
-    }
+    issue_particle_load<K, VT>(&a, pp, buf, tid, lane, tile, stg, &sc.bar, tile_bytes, col_bytes, lflags,
+                               inv_s);
   };
   while (p < a.P) {
     const unsigned q_next = a.work ? claim() : 0u;
@@ -1260,20 +1323,27 @@ step_kernel(const StepArgs a) {
           const double offx = -(xr != lr ? c2r2 : 0.0) - (xr != gr ? c3r3 : 0.0);
           const double offl = c2r2 + (lr == gr ? c3r3 : 0.0);
           auto upd = [&](int r, double off) {
-            const float u = colp[r * n];
-            const float lin = fminf(fmaxf((float)fma(c1sd, (double)u, off), -vm), vm);
-            const float u2 = lin * rc;
+            const float u = colp[r * n];             // wide word
+            const double ud = wdec(u);
+            const float lin = fminf(fmaxf((float)fma(c1sd, ud, off), -vm), vm);
+            const double u2d = (double)lin * (double)rc;
+            const float u2 = wenc(u2d);
             colp[r * n] = u2;
             if (store_v) gcol[r * n] = u2;
-            Ad += (double)fabsf(u2) - (double)fabsf(u);
+            Ad += fabs(wdec(u2)) - fabs(ud);
             if (r == zp) return;
             if (u2 > M) { M = u2; cnt = 1; R = r; }
             else if (u == M) { if (u2 < M && (--cnt == 0 || R == r)) bad = true; }
             else if (u2 == M) { ++cnt; R = min(R, r); }
           };
-          if (offx != 0.0) upd(xr, offx);
-          if (lr != xr) upd(lr, offl);
-          if (gr != xr && gr != lr) upd(gr, c3r3);
+          // the <= 3 touched rows in this order (x, pl, pg), one copy of upd
+#pragma unroll 1
+          for (int j = 0; j < 3; ++j) {
+            const int r = j == 0 ? xr : (j == 1 ? lr : gr);
+            const double off = j == 0 ? offx : (j == 1 ? offl : c3r3);
+            const bool go = j == 0 ? offx != 0.0 : (j == 1 ? lr != xr : (gr != xr && gr != lr));
+            if (go) upd(r, off);
+          }
           if (xr != zp) {
             // the excluded row moves from zp to this step's z row xr
             const float uo = colp[zp * n];
@@ -1321,6 +1391,7 @@ step_kernel(const StepArgs a) {
     }
     auto rescale = [&](VT v, int k) -> VT {
       if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
+      else if constexpr (Wide<VT, G>::value) return wenc(wdec(v) * (double)inv[k]);
       else return v * inv[k];
     };
     float sK[CPL];   // column scale of the tile after this phase (v = u * sK)
@@ -1358,8 +1429,8 @@ step_kernel(const StepArgs a) {
             for (int j = 0; j < CPL; ++j) {
               const int r = lane + j * 32;
               if (r >= n) continue;
-              const float u = (float)tile[r * n + c];
-              sum += (double)fabsf(u);
+              const float u = (float)tile[r * n + c];   // wide word
+              sum += fabs(wdec(u));
               if (r == zc) continue;
               const unsigned key = okey32(__fadd_rn(u, 0.0f));
               if (key > km) { km = key; kc = 1; kr = r; }
@@ -1442,8 +1513,8 @@ step_kernel(const StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
-        nk64[k] = ncnt[k] ? nonz_key(nmax[k], sK[k]) : 0;
-        zkey[k] = z_key(tile[zr[k] * n + col[k]], sK[k]);
+        nk64[k] = ncnt[k] ? nonz_key<VT, G>(nmax[k], sK[k]) : 0;
+        zkey[k] = z_key<VT, G>(tile[zr[k] * n + col[k]], sK[k]);
       }
     }
     if (!GT && do_vel && store_v && !incr) {
@@ -1541,7 +1612,7 @@ step_kernel(const StepArgs a) {
               if (act) {
                 er = sc.srow[ei];
                 ec = sc.sorder[ej];
-                ekey = mkey(tile, sc.sS, n, er, ec, (int)sc.szr[ec]);
+                ekey = mkey<VT, G>(tile, sc.sS, n, er, ec, (int)sc.szr[ec]);
               }
 #pragma unroll 1
               for (int left = kf; left > 0; --left) {
@@ -1829,7 +1900,7 @@ step_kernel(const StepArgs a) {
                     ncnt[k] = (int)tot;
                     nrow[k] = tot ? (int)rr : -1;
                     nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
-                    nk64[k] = tot ? nonz_key(nmax[k], sK[k]) : 0;
+                    nk64[k] = tot ? nonz_key<VT, G>(nmax[k], sK[k]) : 0;
                     recompute(k);
                   }
                 } else {
@@ -1838,7 +1909,7 @@ step_kernel(const StepArgs a) {
                   for (int j = 0; j < CPL; ++j) {
                     const int r = lane + j * 32;
                     if (r >= n || r == zc || !rf.has(r)) continue;
-                    const uint64_t key = nonz_key(tile[r * n + c], 1.0f);
+                    const uint64_t key = nonz_key<VT, G>(tile[r * n + c], 1.0f);
                     if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                     else if (key == rb.key) ++rb.cnt;
                   }
@@ -1869,7 +1940,7 @@ step_kernel(const StepArgs a) {
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
                 if (r >= n || r == zc || !rf.has(r)) continue;
-                const uint64_t key = nonz_key(tile[r * n + c], sc.sS[c]);
+                const uint64_t key = nonz_key<VT, G>(tile[r * n + c], sc.sS[c]);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
               }

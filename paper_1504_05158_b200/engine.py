@@ -237,13 +237,34 @@ class PopulationState:
             self.d_vcol[:, 3].fill_(float("nan"))
             self.d_vcol[:, 4].zero_()
 
+    @property
+    def v_wide(self) -> bool:
+        """fp32 tiles of the one-warp kernels (n <= 64) hold wide 32-bit
+        words: the high word of the float64 value, rounded to nearest (fp32's
+        size, fp64's exponent range; csrc/common.cuh wdec / wenc)."""
+        return self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N
+
+    def v_decode(self, u: torch.Tensor) -> torch.Tensor:
+        """Stored fp32-state words -> float64 values (exact)."""
+        if self.v_wide:
+            return (u.contiguous().view(torch.int32).to(torch.int64) << 32).view(torch.float64)
+        return u.double()
+
+    def v_encode(self, v: torch.Tensor) -> torch.Tensor:
+        """float64 values -> stored fp32-state words (rounded to nearest)."""
+        if self.v_wide:
+            b = (v.contiguous().view(torch.int64) + 0x80000000) >> 32
+            return b.to(torch.int32).view(torch.float32)
+        return v.float()
+
     def set_lazy_scale(self, enabled: bool):
         """Switch the fp32 state to (or from) the lazily scaled layout; V is
-        materialised (u * s, rounded to fp32) when leaving it."""
+        materialised (u * s, rounded to the stored format) when leaving it."""
         if not enabled and self.d_vcol is not None:
             p, n = self.local_particles, self.n
             u = self.d_V[:, :n * n].view(p, n, n)
-            u.mul_(self.d_vcol[:, 0, :n].unsqueeze(1))
+            v = self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)
+            u.copy_(self.v_encode(v))
             self.d_vcol = None
         elif enabled and self.d_vcol is None and self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N:
             self.d_vcol = torch.empty((self.local_particles, 5, _vcs(self.n)), dtype=torch.float32,
@@ -259,7 +280,9 @@ class PopulationState:
         p, n, nn = self.local_particles, self.n, self.n * self.n
         u = self.d_V[:, :nn].view(p, n, n)
         if self.d_vcol is not None:
-            return (u.double() * self.d_vcol[:, 0, :n].double().unsqueeze(1)).cpu().numpy()
+            return (self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)).cpu().numpy()
+        if self.v_wide:
+            return self.v_decode(u).cpu().numpy()
         return u.cpu().numpy()
 
     @property
@@ -373,7 +396,8 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
         perms = perms[lo_p:lo_p + p]
         V = V[lo_p:lo_p + p]
         state.d_perm.copy_(torch.from_numpy(perms.astype(np.int16)))
-        state.d_V[:, :n * n].copy_(torch.from_numpy(V.reshape(p, n * n)))
+        Vt = torch.from_numpy(np.ascontiguousarray(V.reshape(p, n * n), dtype=np.float64))
+        state.d_V[:, :n * n].copy_(state.v_encode(Vt) if state.v_wide else Vt)
         del V
     else:
         _lib.call("qsb_init_population_device", state.c_state(), int(config.seed) & (2**64 - 1),

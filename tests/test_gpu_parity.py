@@ -236,15 +236,15 @@ def _lazy_state_checks(st, n, normalised=True):
     """The lazily scaled layout's column state matches the stored tile."""
     import torch
     p = st.local_particles
-    u = st.d_V[:, :n * n].view(p, n, n).double().cpu().numpy()
+    u = st.v_decode(st.d_V[:, :n * n].view(p, n, n)).cpu().numpy()   # stored words -> values
     vc = st.d_vcol.cpu()
     s = vc[:, 0, :n].double().numpy()
     words = vc.view(torch.int32).numpy().astype(np.int64) & 0xFFFFFFFF
     A = ((words[:, 2, :n] << 32) | words[:, 1, :n]).view(np.float64)
-    M = vc[:, 3, :n].double().numpy()
+    known = ~torch.isnan(vc[:, 3, :n]).numpy()          # NaN word: statistics unknown
+    M = st.v_decode(vc[:, 3, :n]).numpy()
     cr = vc[:, 4, :n].view(torch.int32).numpy()
     assert np.isfinite(s).all() and (s > 0).all()
-    known = ~np.isnan(M)
     zp = cr & 0xFF
     rows = np.arange(n)[None, :, None]
     w = np.where(rows == zp[:, None, :], -np.inf, u)
@@ -355,15 +355,15 @@ def test_fp32_lazy_column_state_invariants(name, steps, c1, golden_instances):
     for _ in range(steps):
         qsb.step(st, inst, cfg)
     n, p = inst.n, st.local_particles
-    u = st.d_V[:, :n * n].view(p, n, n).double().cpu().numpy()
+    u = st.v_decode(st.d_V[:, :n * n].view(p, n, n)).cpu().numpy()   # stored words -> values
     vc = st.d_vcol.cpu()
     s = vc[:, 0, :n].double().numpy()
     words = vc.view(torch.int32).numpy().astype(np.int64) & 0xFFFFFFFF
     A = ((words[:, 2, :n] << 32) | words[:, 1, :n]).view(np.float64)
-    M = vc[:, 3, :n].double().numpy()
+    known = ~torch.isnan(vc[:, 3, :n]).numpy()          # NaN word: statistics unknown
+    M = st.v_decode(vc[:, 3, :n]).numpy()
     cr = vc[:, 4, :n].view(torch.int32).numpy()
     assert np.isfinite(s).all() and (s > 0).all()
-    known = ~np.isnan(M)
     assert known.mean() > 0.9
     zp = cr & 0xFF
     rows = np.arange(n)[None, :, None]
