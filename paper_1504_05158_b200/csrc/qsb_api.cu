@@ -229,6 +229,32 @@ static int launch_twoopt_tc(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
+// n <= 32: four particles per CTA share one MMA batch (twoopt_tc4_kernel)
+static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
+  constexpr int NT = 128;
+  auto fn = twoopt_tc4_kernel<NT>;
+  static int regs = 0, stat = 0;
+  if (!regs) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_status(e);
+    regs = fa.numRegs; stat = (int)fa.sharedSizeBytes;
+  }
+  const size_t smem = 2 * 128 * 32 + align_up((size_t)t.n * (t.n + 1), 16) + 128 * 4 + 128 * 16 + 64;
+  const int warp_regs = (regs * 32 + 255) / 256 * 256;
+  const int by_regs = 65536 / (warp_regs * (NT / 32));
+  const int by_smem = (int)((smem_optin() + 1024) / (smem + stat + 1024));
+  int bps = by_regs < by_smem ? by_regs : by_smem;
+  if (bps > 4) bps = 4;                   // 128 TMEM columns per CTA
+  if (bps < 1) bps = 1;
+  const int64_t groups = (t.P + 3) / 4;
+  const int64_t cap = (int64_t)num_sms() * bps;
+  const int grid = (int)(groups < cap ? groups : cap);
+  if (grid <= 0) return QSB_OK;
+  fn<<<grid, NT, smem, s>>>(t);
+  return launch_status();
+}
+
 static bool twoopt_use_dp4a() {
   static int v = -1;
   if (v < 0) {
@@ -242,7 +268,8 @@ template <typename MT>
 static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = false) {
   if constexpr (sizeof(MT) == 2) {
     if (bytes && t.sym && t.n <= 256 && !twoopt_use_dp4a()) {
-      const int rc = t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
+      const int rc = t.n <= 32 ? launch_twoopt_tc4(t, s)
+                   : t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
       if (rc != QSB_EUNSUPPORTED) return rc;
     }
     if (bytes && t.sym) {

@@ -655,4 +655,208 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
   }
 }
 
+
+// Small instances (n <= 32): four particles per CTA, one warp each, share
+// one MMA batch.  Rows 32 w .. 32 w + 31 of the stacked operands belong to
+// warp w's particle, so
+//   H_stack = [F_4 | P_stack] [P_stack | F_4]^T      (M = N = 128, K = 64)
+// holds every particle's H as a diagonal 32 x 32 block (the off-diagonal
+// blocks are computed and ignored: the tensor core is not the bottleneck
+// here, the per-particle round trips are).  Warp w reads TMEM lanes
+// 32 w .. 32 w + 31 (its lane quarter), columns 32 w .. 32 w + 31, scores
+// its particle's swaps and applies its move itself; the CTA repeats the
+// MMA while any of its particles still moved and passes remain.
+template <int NT>
+__global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
+  static_assert(NT == 128, "one warp per particle, four particles per CTA");
+  constexpr int KB = 32, ROWS = 128;
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  const int n = a.n;
+  const int dn = n + 1;
+  uint8_t* F8 = tsm;                         // 4 stacked copies of F (canonical layout)
+  uint8_t* P8 = F8 + ROWS * KB;              // the 4 particles' P = D[p][p]
+  uint8_t* D8 = P8 + ROWS * KB;              // D row-major, stride n + 1, column n zero
+  int* spall = reinterpret_cast<int*>(D8 + align_up((size_t)n * dn, 16));   // [4][32]
+  int4* svall = reinterpret_cast<int4*>(spall + 128);                          // [4][32]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t s_tmem;
+  __shared__ unsigned s_mx[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
+  const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
+  int* sp = spall + 32 * warp;
+  int4* sv = svall + 32 * warp;
+
+  if (tid < 2) s_mx[tid] = 0;
+  {
+    uint4* z = reinterpret_cast<uint4*>(F8);
+    for (int i = tid; i < 2 * ROWS * KB / 16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  unsigned mf = 0, md = 0;
+  for (int e = tid; e < n * n; e += NT) {
+    const int r = e / n, c = e - r * n;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) F8[cl_off(32 * w + r, c, KB)] = (uint8_t)gF[e];
+    D8[r * dn + c] = (uint8_t)gD[e];
+    mf = max(mf, (unsigned)gF[e]);
+    md = max(md, (unsigned)gD[e]);
+  }
+  for (int r = tid; r < n; r += NT) D8[r * dn + n] = 0;
+  atomicMax(&s_mx[0], mf);
+  atomicMax(&s_mx[1], md);
+  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&s_tmem)), "r"(128) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t idesc = umma_idesc_u8(ROWS, ROWS);
+  const bool narrow = (double)n * (double)s_mx[0] * (double)s_mx[1] < 268435456.0;
+  const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * warp);
+  const int r = lane;                        // this lane's facility (row)
+  uint32_t phase = 0;
+
+  for (int64_t base = (int64_t)blockIdx.x * 4; base < a.P; base += (int64_t)gridDim.x * 4) {
+    const int64_t p = base + warp;
+    const bool valid = p < a.P;
+    __syncwarp();
+    sp[lane] = (valid && lane < n) ? a.perm[p * n + lane] : 0;
+    __syncwarp();
+    {
+      // row r of this particle's P: bytes j < n gathered, the rest zero
+      unsigned w[8];
+      const uint8_t* drow = D8 + sp[r] * dn;
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        unsigned b[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int j = 4 * x + y;
+          b[y] = (valid && r < n && j < n) ? (unsigned)drow[sp[j]] : 0u;
+        }
+        w[x] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+      }
+      *reinterpret_cast<uint4*>(P8 + cl_off(32 * warp + r, 0, KB)) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(P8 + cl_off(32 * warp + r, 16, KB)) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+    uint64_t cost = valid ? (uint64_t)a.cost[p] : 0;
+    bool active = valid && a.passes > 0;
+    for (int pass = 0; pass < a.passes; ++pass) {
+      // G[r][r] and the diagonals of this lane's row
+      {
+        const uint4 f0 = *reinterpret_cast<const uint4*>(F8 + cl_off(32 * warp + r, 0, KB));
+        const uint4 f1 = *reinterpret_cast<const uint4*>(F8 + cl_off(32 * warp + r, 16, KB));
+        const uint4 d0 = *reinterpret_cast<const uint4*>(P8 + cl_off(32 * warp + r, 0, KB));
+        const uint4 d1 = *reinterpret_cast<const uint4*>(P8 + cl_off(32 * warp + r, 16, KB));
+        unsigned acc = 0;
+        acc = __dp4a(f0.x, d0.x, acc); acc = __dp4a(f0.y, d0.y, acc);
+        acc = __dp4a(f0.z, d0.z, acc); acc = __dp4a(f0.w, d0.w, acc);
+        acc = __dp4a(f1.x, d1.x, acc); acc = __dp4a(f1.y, d1.y, acc);
+        acc = __dp4a(f1.z, d1.z, acc); acc = __dp4a(f1.w, d1.w, acc);
+        sv[r] = make_int4((int)acc, F8[cl_off(32 * warp + r, r, KB)], P8[cl_off(32 * warp + r, r, KB)], 0);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t fa = smem_u32(F8), pa = smem_u32(P8);
+        umma_i8(tmem, umma_smem_desc(fa, 128, KB * 8), umma_smem_desc(pa, 128, KB * 8), idesc, 0u);
+        umma_i8(tmem, umma_smem_desc(pa, 128, KB * 8), umma_smem_desc(fa, 128, KB * 8), idesc, 1u);
+        umma_commit(&bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      tc_fence_after();
+      uint32_t v0[16], v1[16];
+      tmem_ld16(trow, v0);
+      tmem_ld16(trow + 16u, v1);
+      tc_fence_before();
+      int bd = INT_MAX, bs = -1;
+      int64_t wbd = INT64_MAX;
+      if (active && r < n) {
+        const int4 mine = sv[r];
+        const int gdr = mine.x, Frr = mine.y, Prr = mine.z;
+        const uint4 fr0 = *reinterpret_cast<const uint4*>(F8 + cl_off(32 * warp + r, 0, KB));
+        const uint4 fr1 = *reinterpret_cast<const uint4*>(F8 + cl_off(32 * warp + r, 16, KB));
+        const uint4 pr0 = *reinterpret_cast<const uint4*>(P8 + cl_off(32 * warp + r, 0, KB));
+        const uint4 pr1 = *reinterpret_cast<const uint4*>(P8 + cl_off(32 * warp + r, 16, KB));
+        const unsigned fw[8] = {fr0.x, fr0.y, fr0.z, fr0.w, fr1.x, fr1.y, fr1.z, fr1.w};
+        const unsigned pw[8] = {pr0.x, pr0.y, pr0.z, pr0.w, pr1.x, pr1.y, pr1.z, pr1.w};
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+          const int4 o = sv[s];
+          const int Frs = (int)__byte_perm(fw[s >> 2], 0u, 0x4440 | (s & 3));
+          const int Prs = (int)__byte_perm(pw[s >> 2], 0u, 0x4440 | (s & 3));
+          const int t = (2 * Frs - Frr - o.y) * (2 * Prs - Prr - o.z);
+          const uint32_t h = s < 16 ? v0[s & 15] : v1[s & 15];
+          const bool ok = s > r && s < n;
+          if (narrow) {
+            const int dd = 2 * ((int)h - gdr - o.x) + t;
+            if (ok && dd < bd) { bd = dd; bs = s; }
+          } else {
+            const int64_t dd = 2 * ((int64_t)h - gdr - o.x) + t;
+            if (ok && dd < wbd) { wbd = dd; bs = s; }
+          }
+        }
+      }
+      int64_t best = bs < 0 ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
+      int bq = bs < 0 ? INT_MAX : r * n - r * (r + 1) / 2 + (bs - r - 1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      if (active && bq != INT_MAX && best < 0) {
+        cost += (uint64_t)best;
+        int r0, s0;
+        unrank_pair(bq, n, r0, s0);
+        // swap facilities r0 and s0 of this warp's P: rows, then columns
+        if (lane < KB) {
+          const int ir = cl_off(32 * warp + r0, lane, KB), is = cl_off(32 * warp + s0, lane, KB);
+          const uint8_t x = P8[ir]; P8[ir] = P8[is]; P8[is] = x;
+        }
+        __syncwarp();
+        {
+          const int ir = cl_off(32 * warp + lane, r0, KB), is = cl_off(32 * warp + lane, s0, KB);
+          const uint8_t x = P8[ir]; P8[ir] = P8[is]; P8[is] = x;
+        }
+        if (lane == 0) { const int x = sp[r0]; sp[r0] = sp[s0]; sp[s0] = x; }
+        __syncwarp();
+      } else {
+        active = false;
+      }
+      // another pass only while some particle of the CTA still moved
+      if (!__syncthreads_or(active)) break;
+    }
+    __syncwarp();
+    if (valid) {
+      if (lane < n) a.perm[p * n + lane] = (int16_t)sp[lane];
+      bool imp = false;
+      if (a.do_pbest) {
+        imp = (int64_t)cost < a.pl_cost[p];
+        if (lane == 0) {
+          if (imp) a.pl_cost[p] = (int64_t)cost;
+          a.improved[p] = imp ? 1 : 0;
+        }
+        if (imp && lane < n) a.pl_perm[p * n + lane] = (int16_t)sp[lane];
+      }
+      if (lane == 0) a.cost[p] = (int64_t)cost;
+    }
+    __syncthreads();   // P8 / sp reused by the next group
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(128) : "memory");
+  }
+}
+
 }  // namespace qsb
