@@ -72,7 +72,12 @@ typedef struct qsb_state {
   int64_t num_swarms;        /* swarms on this device */
   int64_t particle_offset;   /* global id of local particle 0 */
   int64_t swarm_offset;      /* global id of local swarm 0 */
-  void* V;                   /* (P, vstride) */
+  void* V;                   /* (P, vstride).  QSB_F64: doubles.  QSB_F32 in
+                              * the lazily scaled layout (vcol set): "wide"
+                              * 32-bit words, the high word of the double
+                              * (sign, 11-bit exponent, 20-bit fraction)
+                              * rounded to nearest (fp64's exponent range in
+                              * fp32's size); QSB_F32 otherwise: floats. */
   int16_t* perm;             /* (P, n) current position X */
   int16_t* perm_new;         /* (P, n) next position */
   int16_t* pl_perm;          /* (P, n) personal best PL */
@@ -95,7 +100,7 @@ typedef struct qsb_state {
    * per column; vcol is (P, 5, vcs) 32-bit words with vcs = n rounded up to
    * a multiple of 4: row 0 the column scale s (f32), rows 1-2 the low / high
    * words of the f64 sum of |u| over the column, row 3 the maximum of u over
-   * the rows other than zp (f32, NaN = unknown), row 4 (int32) count << 16 |
+   * the rows other than zp (a wide word, NaN = unknown), row 4 (int32) count << 16 |
    * first row << 8 | zp, zp being the z row (the position) of the step that
    * wrote them.  Set row 0 to 1 and row 3 to NaN whenever V is written from
    * outside the step. */

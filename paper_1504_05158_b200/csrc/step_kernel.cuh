@@ -173,6 +173,7 @@ struct GroupScratch {
   uint8_t szr[NMAX];     // perm of the current position X (z row per column)
   uint8_t sorder[NMAX];  // pick-column visiting order
   unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
+  bool wide;                 // tile entries are wide words (lazily scaled fp32 layout)
 };
 
 template <int G>
@@ -259,42 +260,32 @@ __device__ __forceinline__ int group_min_int(int x, Scratch& sc, int& ipar, int 
 }
 
 // Velocity value of a stored entry.  fp64 tiles hold v itself.  fp32 tiles
-// of the one-warp kernels (G == 1) hold "wide" 32-bit words: the high word
-// of the double (sign, 11-bit exponent, 20-bit fraction), rounded to
-// nearest -- the byte size of fp32 with the exponent range of fp64, so an
-// entry the reference keeps as a tiny non-zero value (it decays by ~1 bit
-// per step while x / pl / pg leave it alone) does not flush to zero after
-// ~150 steps as an fp32 would, and does not turn into a spurious tie.  The
-// words order like floats (sign-magnitude), so stored values are compared
-// with float compares on the raw bits (exact for |v| in [2^-1015, 2^1017];
-// no flush-to-zero in this build).  Multi-warp fp32 tiles hold plain
-// floats.  Lazily scaled: v = u * s (s the column scale, 1.0 otherwise);
-// the product is exact in double.
-template <typename VT, int G>
-struct Wide { static constexpr bool value = sizeof(VT) == 4 && G == 1; };
-
-template <typename VT, int G>
-__device__ __forceinline__ double vdec(VT u) {   // stored word -> value (unscaled)
-  if constexpr (Wide<VT, G>::value) return wdec(u);
-  else return (double)u;
-}
-template <typename VT, int G>
-__device__ __forceinline__ VT venc(double v) {   // value -> stored word
-  if constexpr (Wide<VT, G>::value) return wenc(v);
-  else return (VT)v;
-}
-template <typename VT, int G>
-__device__ __forceinline__ double vval(VT u, float s) {
+// in the lazily scaled layout hold "wide" 32-bit words: the high word of the
+// double (sign, 11-bit exponent, 20-bit fraction), rounded to nearest -- the
+// byte size of fp32 with the exponent range of fp64, so an entry the
+// reference keeps as a tiny non-zero value (it decays by ~1 bit per step
+// while x / pl / pg leave it alone) does not flush to zero after ~150 steps
+// as an fp32 would, and does not turn into a spurious tie.  The words order
+// like floats (sign-magnitude), so stored values are compared with float
+// compares on the raw bits (exact for |v| in [2^-1015, 2^1017]; no
+// flush-to-zero in this build).  Stored-v fp32 tiles hold plain floats.
+// Lazily scaled: v = u * s (s the column scale, 1.0 otherwise); the product
+// is exact in double.
+// `wide` is a runtime property of the state: true for the lazily scaled
+// layout of the one-warp fp32 kernels, false for stored-v fp32 tiles (the
+// streaming velocity pass keeps float arithmetic) and for fp64.
+template <typename VT>
+__device__ __forceinline__ double vval(VT u, float s, bool wide) {
   if constexpr (sizeof(VT) == 8) return u;
-  else return vdec<VT, G>(u) * (double)s;
+  else return (wide ? wdec(u) : (double)u) * (double)s;
 }
-template <typename VT, int G>
-__device__ __forceinline__ uint64_t nonz_key(VT v, float s) {   // key of m = 0.0 + v
-  return okey(__dadd_rn(0.0, vval<VT, G>(v, s)));
+template <typename VT>
+__device__ __forceinline__ uint64_t nonz_key(VT v, float s, bool wide) {   // key of m = 0.0 + v
+  return okey(__dadd_rn(0.0, vval(v, s, wide)));
 }
-template <typename VT, int G>
-__device__ __forceinline__ uint64_t z_key(VT v, float s) {      // key of m = 1.0 + v
-  return okey(__dadd_rn(1.0, vval<VT, G>(v, s)));
+template <typename VT>
+__device__ __forceinline__ uint64_t z_key(VT v, float s, bool wide) {      // key of m = 1.0 + v
+  return okey(__dadd_rn(1.0, vval(v, s, wide)));
 }
 
 // Set of free rows (bit r of word r/64).
@@ -310,9 +301,10 @@ struct RowSet {
   }
 };
 
-template <typename VT, int G>
-__device__ __forceinline__ uint64_t mkey(const VT* tile, const float* sS, int n, int r, int c, int zrc) {
-  return okey(__dadd_rn(r == zrc ? 1.0 : 0.0, vval<VT, G>(tile[r * n + c], sS[c])));
+template <typename VT>
+__device__ __forceinline__ uint64_t mkey(const VT* tile, const float* sS, int n, int r, int c, int zrc,
+                                         bool wide) {
+  return okey(__dadd_rn(r == zrc ? 1.0 : 0.0, vval(tile[r * n + c], sS[c], wide)));
 }
 
 // ---- rare paths, kept out of line so the round loop stays in I-cache ----
@@ -348,7 +340,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
         if (!tf) continue;
         const int zc = sc.szr[c];
         if (r == zc && tf != 2) continue;
-        if (mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) ++cnt;
+        if (mkey(tile, sc.sS, n, r, c, zc, sc.wide) == key) ++cnt;
       }
     }
     sc.srow[r] = cnt;
@@ -363,7 +355,7 @@ __device__ __noinline__ void tie_select_slow(const VT* tile, int n, Scratch& sc,
       if (!tf) continue;
       const int zc = sc.szr[c];
       if (r == zc && tf != 2) continue;
-      if (mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) {
+      if (mkey(tile, sc.sS, n, r, c, zc, sc.wide) == key) {
         if (q == 0) { cc = c; break; }
         --q;
       }
@@ -382,7 +374,7 @@ __device__ __noinline__ int first_row_scan(const VT* tile, int n, Scratch& sc, R
   const int zc = sc.szr[c];
   int found = INT_MAX;
   for (int r = tid; r < n; r += NT)
-    if (rf.has(r) && (r != zc || zok) && mkey<VT, G>(tile, sc.sS, n, r, c, zc) == key) found = min(found, r);
+    if (rf.has(r) && (r != zc || zok) && mkey(tile, sc.sS, n, r, c, zc, sc.wide) == key) found = min(found, r);
   return group_min_sync<G>(found, sc, lane, tid);
 }
 
@@ -455,8 +447,8 @@ __device__ __noinline__ int tie_select_warp(const VT* tile, int n, Scratch& sc, 
       b &= b - 1;
       const int zc = sc.szr[c];
       const bool zok = sc.stie[c] == 2;
-      const bool a0 = r0ok && (c0 != zc || zok) && mkey<VT, 1>(tile, sc.sS, n, c0, c, zc) == key;
-      const bool a1 = r1ok && (c1 != zc || zok) && mkey<VT, 1>(tile, sc.sS, n, c1, c, zc) == key;
+      const bool a0 = r0ok && (c0 != zc || zok) && mkey(tile, sc.sS, n, c0, c, zc, sc.wide) == key;
+      const bool a1 = r1ok && (c1 != zc || zok) && mkey(tile, sc.sS, n, c1, c, zc, sc.wide) == key;
       const unsigned m0 = __ballot_sync(FULL, a0), m1 = __ballot_sync(FULL, a1);
       cnt0 += a0;
       cnt1 += a1;
@@ -517,7 +509,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
     Best rb = best_none();
     for (int r = tid; r < n; r += NT) {
       if (!rf.has(r)) continue;
-      const uint64_t key = mkey<VT, G>(tile, sc.sS, n, r, c, zc);
+      const uint64_t key = mkey(tile, sc.sS, n, r, c, zc, sc.wide);
       if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
       else if (key == rb.key) ++rb.cnt;
     }
@@ -528,7 +520,7 @@ __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc,
       const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
       const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
       for (int r = tid; r < n; r += NT)
-        sc.srow[r] = (rf.has(r) && mkey<VT, G>(tile, sc.sS, n, r, c, zc) == b.key) ? 1 : 0;
+        sc.srow[r] = (rf.has(r) && mkey(tile, sc.sS, n, r, c, zc, sc.wide) == b.key) ? 1 : 0;
       GroupSync<G>::sync();
       if (tid == 0) {
         int q = pick, r = 0;
@@ -622,7 +614,6 @@ __device__ __noinline__ ColOut<VT, CPL> stats_generic(VT* tile, int n, const Col
       VT v = *cell;
       if (in.scale[k]) {
         if constexpr (sizeof(VT) == 8) v = __ddiv_rn(v, in.total[k]);
-        else if constexpr (Wide<VT, G>::value) v = wenc(wdec(v) * (double)in.inv[k]);
         else v = v * in.inv[k];
         *cell = v;
       }
@@ -655,7 +646,6 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
   }
   auto rescale = [&](VT v, int k) -> VT {
     if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
-    else if constexpr (Wide<VT, G>::value) return wenc(wdec(v) * (double)inv[k]);
     else return v * inv[k];
   };
   // Max / tie count / first row over the non-z rows (the z row is masked
@@ -694,7 +684,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
       const int n2 = 2 * n;
       auto sc_ = [&](VT v, VT f, int k) -> VT {
         if constexpr (sizeof(VT) == 8) return k == 0 || live1 ? __ddiv_rn(v, total[k]) : v;
-        else return wenc(wdec(v) * (double)f);   // G == 1 here: wide words
+        else return v * f;
       };
       auto upd2 = [&](VT w, int r, int, VT& m, int& c, int& rr) {
         const bool gt = w > m;
@@ -732,7 +722,7 @@ __device__ __noinline__ ColOut<VT, CPL> stats_pass(VT* tile, int n, const ColIn<
     }
     // batches of 8 rows, loads first (latency-bound walk for GT tiles);
     // even rows feed the first chain, odd rows the second, as below
-    constexpr int RB = 8;
+    constexpr int RB = G >= 8 ? 16 : 8;   // deeper for the global-memory tiles (n > 128)
     int r = 0;
     for (; r + RB <= n; r += RB) {
 #pragma unroll
@@ -816,10 +806,12 @@ struct VelOut { float total[CPL]; };
 
 template <int G, int CPL>
 __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn<CPL> in, double c1,
-                                                 double c2r2, double c3r3, double vmax, int v_bounded) {
-  // G == 1: the tile holds wide words (see wdec / wenc), decoded to double,
-  // scaled and clamped in double, re-encoded; G > 1: plain floats
-  constexpr bool WF = G == 1;
+                                                 double c2r2, double c3r3, double vmax, int v_bounded,
+                                                 bool wide) {
+  // wide (the lazily scaled layout): the tile holds wide words (wdec /
+  // wenc), decoded to double, scaled and clamped in double, re-encoded;
+  // otherwise plain floats in float arithmetic
+  const bool WF = wide;
   VelOut<CPL> o;
   int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
   bool cfree[CPL];
@@ -861,7 +853,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   // one stored word scaled by the column factor and clamped; returns the
   // word to store, and the value's magnitude for the column sum
   auto step1 = [&](float w, int k, float f, double fd, float& mag) -> float {
-    if constexpr (WF) {
+    if (WF) {
       const double x = fmin(fmax(fd * wdec(w), -vmcd), vmcd);
       mag = (float)fabs(x);
       return wenc(x);
@@ -886,20 +878,42 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
         if constexpr (decltype(clampit)::value) return fmin(fmax(x, -vmcd), vmcd);
         else return x;
       };
+      auto clf = [&](float x) -> float {
+        if constexpr (decltype(clampit)::value) return fminf(fmaxf(x, -vmc), vmc);
+        else return x;
+      };
       int r = 0;
-      for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
-        const double a0 = cl(f0 * wdec(q0[0])), a1 = cl(f0 * wdec(q0[n]));
-        q0[0] = wenc(a0); q0[n] = wenc(a1);
-        tot[0] += (float)fabs(a0); tot2[0] += (float)fabs(a1);
-        const double b0 = cl(f1 * wdec(q1[0])), b1 = cl(f1 * wdec(q1[n]));
-        q1[0] = wenc(b0); q1[n] = wenc(b1);
-        tot[1] += (float)fabs(b0); tot2[1] += (float)fabs(b1);
-      }
-      if (r < n) {
-        const double a0 = cl(f0 * wdec(q0[0]));
-        q0[0] = wenc(a0); tot[0] += (float)fabs(a0);
-        const double b0 = cl(f1 * wdec(q1[0]));
-        q1[0] = wenc(b0); tot[1] += (float)fabs(b0);
+      if (WF) {
+        for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+          const double a0 = cl(f0 * wdec(q0[0])), a1 = cl(f0 * wdec(q0[n]));
+          q0[0] = wenc(a0); q0[n] = wenc(a1);
+          tot[0] += (float)fabs(a0); tot2[0] += (float)fabs(a1);
+          const double b0 = cl(f1 * wdec(q1[0])), b1 = cl(f1 * wdec(q1[n]));
+          q1[0] = wenc(b0); q1[n] = wenc(b1);
+          tot[1] += (float)fabs(b0); tot2[1] += (float)fabs(b1);
+        }
+        if (r < n) {
+          const double a0 = cl(f0 * wdec(q0[0]));
+          q0[0] = wenc(a0); tot[0] += (float)fabs(a0);
+          const double b0 = cl(f1 * wdec(q1[0]));
+          q1[0] = wenc(b0); tot[1] += (float)fabs(b0);
+        }
+      } else {
+        const float g0 = c1k[0], g1 = live1 ? c1k[1] : 1.0f;
+        for (; r + 1 < n; r += 2, q0 += n2, q1 += n2) {
+          const float a0 = clf(g0 * q0[0]), a1 = clf(g0 * q0[n]);
+          q0[0] = a0; q0[n] = a1;
+          tot[0] += fabsf(a0); tot2[0] += fabsf(a1);
+          const float b0 = clf(g1 * q1[0]), b1 = clf(g1 * q1[n]);
+          q1[0] = b0; q1[n] = b1;
+          tot[1] += fabsf(b0); tot2[1] += fabsf(b1);
+        }
+        if (r < n) {
+          const float a0 = clf(g0 * q0[0]);
+          q0[0] = a0; tot[0] += fabsf(a0);
+          const float b0 = clf(g1 * q1[0]);
+          q1[0] = b0; tot[1] += fabsf(b0);
+        }
       }
     };
     if (v_bounded) run(std::false_type{});
@@ -907,7 +921,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   } else {
     // batches of 8 rows, loads first: with the tile in global memory (GT)
     // the column walk is latency-bound unless many loads are in flight
-    constexpr int RB = 8;
+    constexpr int RB = G >= 8 ? 16 : 8;   // deeper for the global-memory tiles (n > 128)
     int r = 0;
     for (; r + RB <= n; r += RB) {
 #pragma unroll
@@ -952,7 +966,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
       (void)step1(v0, k, c1k[k], c1kd[k], gmag);
       const double vd = WF ? wdec(v0) : (double)v0;
       const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * (vd * (double)cs[k])));
-      if constexpr (WF) {
+      if (WF) {
         const double sp = fmin(fmax(l, -vmax), vmax);
         colp[r * n] = wenc(sp);
         tot[k] += (float)fabs(sp) - gmag;
@@ -1033,6 +1047,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   // per column that x / pl / pg touch ("lazy column scale").
   constexpr bool kLazy = sizeof(VT) == 4 && G == 1 && !GT;
   const bool lazy = kLazy && a.vcol != nullptr;
+  const bool wide = lazy;   // lazily scaled fp32 tiles hold wide words (vval)
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
@@ -1071,6 +1086,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   }
   if (tid == 0) { mbar_init(&sc.bar, 1); mbar_fence_init(); }
   for (int c = tid; c < K::NMAX; c += NT) { sc.stie[c] = 0; sc.sS[c] = 1.0f; }
+  if (tid == 0) sc.wide = wide;
   __syncthreads();
 
   const uint64_t t = a.t_dev ? (uint64_t)(*a.t_dev) + 1 : a.t_host;
@@ -1254,7 +1270,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
         for (int k = 0; k < CPL; ++k) tot[k] = 0.0;
         // loads issued 8 rows ahead (GT tiles live in global memory); the
         // arithmetic and the column sum stay in row order
-        constexpr int RB = 8;
+        constexpr int RB = GT ? 16 : 8;
         double xb[CPL][RB];
         for (int r = 0; r < n; ++r) {
           if ((r & (RB - 1)) == 0) {
@@ -1368,7 +1384,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k];
         }
         const VelOut<CPL> vo = vel_full_f32<G, CPL>(reinterpret_cast<float*>(tile), n, vi, a.c1, c2r2,
-                                                    c3r3, a.vmax, a.v_bounded);
+                                                    c3r3, a.vmax, a.v_bounded, wide);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) total[k] = (VT)vo.total[k];
       }
@@ -1391,7 +1407,6 @@ step_kernel(const __grid_constant__ StepArgs a) {
     }
     auto rescale = [&](VT v, int k) -> VT {
       if constexpr (sizeof(VT) == 8) return __ddiv_rn(v, total[k]);
-      else if constexpr (Wide<VT, G>::value) return wenc(wdec(v) * (double)inv[k]);
       else return v * inv[k];
     };
     float sK[CPL];   // column scale of the tile after this phase (v = u * sK)
@@ -1477,7 +1492,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       for (int k = 0; k < CPL; ++k) { nmax[k] = so.m[k]; ncnt[k] = so.c[k]; nrow[k] = so.r[k]; }
     } else if (!lazy) {
       // normalisation only (no aggregation): batches of 8 rows, loads first
-      constexpr int RB = 8;
+      constexpr int RB = GT ? 16 : 8;
       int r = 0;
 #pragma unroll 1
       for (; r + RB <= n; r += RB) {
@@ -1513,8 +1528,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
-        nk64[k] = ncnt[k] ? nonz_key<VT, G>(nmax[k], sK[k]) : 0;
-        zkey[k] = z_key<VT, G>(tile[zr[k] * n + col[k]], sK[k]);
+        nk64[k] = ncnt[k] ? nonz_key(nmax[k], sK[k], wide) : 0;
+        zkey[k] = z_key(tile[zr[k] * n + col[k]], sK[k], wide);
       }
     }
     if (!GT && do_vel && store_v && !incr) {
@@ -1612,7 +1627,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
               if (act) {
                 er = sc.srow[ei];
                 ec = sc.sorder[ej];
-                ekey = mkey<VT, G>(tile, sc.sS, n, er, ec, (int)sc.szr[ec]);
+                ekey = mkey(tile, sc.sS, n, er, ec, (int)sc.szr[ec], sc.wide);
               }
 #pragma unroll 1
               for (int left = kf; left > 0; --left) {
@@ -1900,7 +1915,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                     ncnt[k] = (int)tot;
                     nrow[k] = tot ? (int)rr : -1;
                     nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
-                    nk64[k] = tot ? nonz_key<VT, G>(nmax[k], sK[k]) : 0;
+                    nk64[k] = tot ? nonz_key(nmax[k], sK[k], wide) : 0;
                     recompute(k);
                   }
                 } else {
@@ -1909,7 +1924,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                   for (int j = 0; j < CPL; ++j) {
                     const int r = lane + j * 32;
                     if (r >= n || r == zc || !rf.has(r)) continue;
-                    const uint64_t key = nonz_key<VT, G>(tile[r * n + c], 1.0f);
+                    const uint64_t key = nonz_key(tile[r * n + c], 1.0f, false);
                     if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                     else if (key == rb.key) ++rb.cnt;
                   }
@@ -1940,7 +1955,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
                 if (r >= n || r == zc || !rf.has(r)) continue;
-                const uint64_t key = nonz_key<VT, G>(tile[r * n + c], sc.sS[c]);
+                const uint64_t key = nonz_key(tile[r * n + c], sc.sS[c], false);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
               }

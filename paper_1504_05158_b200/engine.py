@@ -239,10 +239,11 @@ class PopulationState:
 
     @property
     def v_wide(self) -> bool:
-        """fp32 tiles of the one-warp kernels (n <= 64) hold wide 32-bit
-        words: the high word of the float64 value, rounded to nearest (fp32's
-        size, fp64's exponent range; csrc/common.cuh wdec / wenc)."""
-        return self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N
+        """Lazily scaled fp32 tiles hold wide 32-bit words: the high word of
+        the float64 value, rounded to nearest (fp32's size, fp64's exponent
+        range; csrc/common.cuh wdec / wenc).  Stored-v fp32 tiles hold
+        floats."""
+        return self.v_code == _lib.F32 and getattr(self, "d_vcol", None) is not None
 
     def v_decode(self, u: torch.Tensor) -> torch.Tensor:
         """Stored fp32-state words -> float64 values (exact)."""
@@ -264,11 +265,14 @@ class PopulationState:
             p, n = self.local_particles, self.n
             u = self.d_V[:, :n * n].view(p, n, n)
             v = self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)
-            u.copy_(self.v_encode(v))
-            self.d_vcol = None
+            self.d_vcol = None                # stored-v: plain floats
+            u.copy_(v.float())
         elif enabled and self.d_vcol is None and self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N:
-            self.d_vcol = torch.empty((self.local_particles, 5, _vcs(self.n)), dtype=torch.float32,
-                                      device=self.device)
+            p, n = self.local_particles, self.n
+            u = self.d_V[:, :n * n].view(p, n, n)
+            v = u.double()
+            self.d_vcol = torch.empty((p, 5, _vcs(n)), dtype=torch.float32, device=self.device)
+            u.copy_(self.v_encode(v))         # lazily scaled: wide words
             self.reset_vcol()
         self._cs = None
         self._graph_cache = None
@@ -281,8 +285,6 @@ class PopulationState:
         u = self.d_V[:, :nn].view(p, n, n)
         if self.d_vcol is not None:
             return (self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)).cpu().numpy()
-        if self.v_wide:
-            return self.v_decode(u).cpu().numpy()
         return u.cpu().numpy()
 
     @property

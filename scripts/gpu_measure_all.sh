@@ -20,3 +20,9 @@ import json,sys
 d=json.load(open('$f')); r=d.get('roofline') or {}
 print(round(d['value']), 'ms', round(d.get('ms_per_step',0),4), 'kern', r.get('kernel_ms'), 'frac', r.get('frac'), 'e2e', (d.get('e2e') or {}).get('value'))")"; done
 tail -3 gpurun_out/m/err.log
+# 2-opt kernels (tensor cores): launch lists of configs 2 / 5 and one full capture each
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m/launches_c2.csv python bench.py --preset config2 --steps 5 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/m/ncu_launch_c2.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m/launches_c5.csv python bench.py --preset config5 --steps 3 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/m/ncu_launch_c5.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:twoopt_tc -s 2 -c 1 -o gpurun_out/m/prof_twoopt_c5 python bench.py --preset config5 --no-cpu --steps 3 --warmup 3 --e2e-steps 0 > gpurun_out/m/ncu_to5.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:twoopt_tc -s 2 -c 1 -o gpurun_out/m/prof_twoopt_c2 python bench.py --preset config2 --no-cpu --steps 3 --warmup 3 --e2e-steps 0 > gpurun_out/m/ncu_to2.log 2>&1
+bash scripts/gpu_velocity_sweep.sh > gpurun_out/m/velocity_sweep.log 2>&1
