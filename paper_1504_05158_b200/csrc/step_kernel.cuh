@@ -1491,8 +1491,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) { nmax[k] = so.m[k]; ncnt[k] = so.c[k]; nrow[k] = so.r[k]; }
     } else if (!lazy) {
-      // normalisation only (no aggregation): batches of 8 rows, loads first
-      constexpr int RB = GT ? 16 : 8;
+      // normalisation only (no aggregation): batches of 16 rows, loads first
+      constexpr int RB = 16;
       int r = 0;
 #pragma unroll 1
       for (; r + RB <= n; r += RB) {
