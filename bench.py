@@ -192,6 +192,24 @@ class KernelTimer:
         d = [a.elapsed_time(b) for a, b in self.pairs]
         return sum(d) / len(d) if d else None
 
+    # the 2-opt launch (tensor cores), when the config runs one
+    def before_twoopt(self, stream):
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.torch.cuda.current_stream())
+            self.pairs2 = getattr(self, "pairs2", [])
+            self.pairs2.append([e, None])
+
+    def after_twoopt(self, stream):
+        if self.active:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.torch.cuda.current_stream())
+            self.pairs2[-1][1] = e
+
+    def mean_twoopt_ms(self):
+        d = [a.elapsed_time(b) for a, b in getattr(self, "pairs2", [])]
+        return sum(d) / len(d) if d else None
+
 
 def traffic_from_profile(n, precision, particles, prefix=""):
     """ncu DRAM bytes per launch of the fused kernel, from profiles/ (or None)."""
@@ -425,6 +443,28 @@ def main():
                 "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"}
 
+    # ---- the 2-opt kernel's tensor-core roofline (configs with 2-opt):
+    # algorithmic work of a pass is the GEMM H = [F|P][P|F]^T, 2 * n * n * 2n
+    # ops per particle; peak = 2 x the measured dense bf16 rate (B200's dense
+    # int8 rate is twice its bf16 rate)
+    roofline2 = None
+    t2 = timer.mean_twoopt_ms()
+    if args.two_opt and t2:
+        ops = 4.0 * args.n ** 3 * state.local_particles * args.two_opt
+        bf16 = peaks.get("bf16_tflops")
+        peak2 = 2.0 * bf16 if bf16 else 4500.0
+        tmax = torch.tensor([t2], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        ach2 = ops / (float(tmax[0]) / 1000.0) / 1e12
+        roofline2 = {"bound": "tensor", "achieved": ach2, "peak": peak2, "unit": "TOP/s",
+                     "frac": ach2 / peak2, "traffic": None,
+                     "kernel": "twoopt_tc kernels (tcgen05.mma kind::i8, u8 x u8 -> s32)",
+                     "kernel_ms": float(tmax[0]),
+                     "algorithmic_ops_per_launch": ops,
+                     "note": "upper bound on passes (a particle stops early when no swap improves)",
+                     "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops" if bf16 else "nominal int8 dense"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(args, args.cpu_seconds)
@@ -440,6 +480,7 @@ def main():
                 "dtype": "f32" if cfg.precision == "fp32" else "f64", "data": "synthetic",
                 "config": workload(args, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clock_rec,
+                "roofline_twoopt": roofline2,
                 "best_cost": best.cost if best else state.best_cost}
         if flags is not None:
             line["metric"] = "velocity/normalise phase HBM throughput"

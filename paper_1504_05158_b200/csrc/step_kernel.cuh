@@ -1268,12 +1268,12 @@ step_kernel(const __grid_constant__ StepArgs a) {
         double tot[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) tot[k] = 0.0;
-        // loads issued 8 rows ahead (GT tiles live in global memory); the
+        // GT tiles (global memory): loads issued 16 rows ahead; the
         // arithmetic and the column sum stay in row order
-        constexpr int RB = GT ? 16 : 8;
+        constexpr int RB = GT ? 16 : 1;
         double xb[CPL][RB];
         for (int r = 0; r < n; ++r) {
-          if ((r & (RB - 1)) == 0) {
+          if (GT && (r & (RB - 1)) == 0) {
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
               if (!cfree[k]) continue;
@@ -1287,7 +1287,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
             if (!cfree[k]) continue;
             const int xr = zr[k], lr = plr[k], gr = pgr[k];
             double* cell = tile + r * n + col[k];
-            double v = xb[k][0];
+            double v = GT ? xb[k][0] : *cell;   // smem tiles: direct loads
 #pragma unroll
             for (int b = 1; b < RB; ++b) if ((r & (RB - 1)) == b) v = xb[k][b];
             const bool special = r == xr || r == lr || r == gr;

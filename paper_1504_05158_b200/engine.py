@@ -606,7 +606,12 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     if passes:
         tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
               | (_lib.TWOOPT_BYTES if rt.twoopt_bytes else 0))
+        tb = getattr(timer, "before_twoopt", None) if timer is not None else None
+        if tb is not None:
+            tb(stream)
         _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, stream)
+        if tb is not None:
+            timer.after_twoopt(stream)
         state.launches += 1
     _lib.call("qsb_best_update", cs, stream)
     state.launches += 3      # draw pre-pass + fused step + best update
