@@ -1,5 +1,5 @@
 """Group an ncu source page of the fused step kernel by phase (marker
-comments in step_kernel.cuh).  Usage: ncu_phase_summary.py REPORT [SRC]"""
+comments in step_kernel.cuh).  Usage: ncu_phase_summary.py REPORT|SOURCE.csv [SRC]"""
 import csv, io, subprocess, sys
 from collections import defaultdict
 
@@ -21,7 +21,7 @@ markers = [("setup", "// ---- per-column registers"),
            ("pbest", "// ================= phase 4a"),
            ]
 bounds = []
-kstart = next(i for i, l in enumerate(lines) if l.startswith("step_kernel(const StepArgs a)")) + 1
+kstart = next(i for i, l in enumerate(lines) if l.startswith("step_kernel(const")) + 1
 for name, m in markers:
     idx = next((i for i, l in enumerate(lines) if m in l), None)
     if idx is not None:
@@ -41,8 +41,11 @@ def region(fname, ln):
     return name
 
 
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv"):      # an exported source page (--print-source cuda,sass)
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 ins = defaultdict(int)
 smp = defaultdict(int)
 fname, hdr = None, None
