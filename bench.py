@@ -108,11 +108,17 @@ def bytes_per_particle(n, S, sv, lazy=False, incremental_cost=True):
     and the column state is read and written (2 * 20 * ceil4(n)).  Both:
     perm / pl_perm read + perm_new write (6n), swarm best row amortised
     (2n/S), (c2 r2, c3 r3) written by the draw pre-pass and read (32), cost
-    read (incremental goal) and written, pl_cost read, improved flag (25)."""
+    read (incremental goal) and written, pl_cost read, improved flag (25).
+    fp32 with n > 64 (deferred column normalisation): V read + write and the
+    n column scales read + written."""
     common = 6 * n + 2 * n / S + 32 + (25 if incremental_cost else 17)
-    if lazy:
+    if lazy and n <= 64:
         vcs = (n + 3) // 4 * 4
         return 4 * n * n + 12 * n + 40 * vcs + common
+    if lazy:
+        # n > 64, fp32: deferred column normalisation (V read + write once,
+        # the column scales read and written)
+        return 2 * n * n * sv + 8 * n + common
     return 2 * n * n * sv + common
 
 
@@ -426,7 +432,8 @@ def main():
     lazy = getattr(state, "d_vcol", None) is not None
     B = bytes_per_particle(args.n, args.swarm_size, sv, lazy=lazy)
     if flags is not None:
-        B = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
+        B = (2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
+             + (8 * args.n if (sv == 4 and args.n > 64) else 0))   # deferred column scales
     per_launch = B * state.local_particles
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"

@@ -103,7 +103,9 @@ typedef struct qsb_state {
    * the rows other than zp (a wide word, NaN = unknown), row 4 (int32) count << 16 |
    * first row << 8 | zp, zp being the z row (the position) of the step that
    * wrote them.  Set row 0 to 1 and row 3 to NaN whenever V is written from
-   * outside the step. */
+   * outside the step.  For n > 64 (multi-warp kernels) only row 0 is used:
+   * the deferred column normalisation, V holds the unnormalised velocity u
+   * (floats) and v = u * s. */
   float* vcol;
   /* (P, 2) scratch for the step's per-particle (c2 * r2, c3 * r3), drawn by a
    * one-thread-per-particle pre-pass; NULL = drawn inside the step kernel. */

@@ -1048,6 +1048,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
   constexpr bool kLazy = sizeof(VT) == 4 && G == 1 && !GT;
   const bool lazy = kLazy && a.vcol != nullptr;
   const bool wide = lazy;   // lazily scaled fp32 tiles hold wide words (vval)
+  // multi-warp fp32 kernels with a column-scale array: deferred column
+  // normalisation -- the tile keeps the unnormalised velocity u and row 0
+  // of vcol the column scale s (v = u * s), so a step reads and writes every
+  // entry once, with no second (rescale) pass over the tile
+  const bool defer = sizeof(VT) == 4 && G > 1 && a.vcol != nullptr;
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
@@ -1208,6 +1213,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       cs[k] = 1.0f; cA[k] = 0.0; cM[k] = 0.0f; cCR[k] = 0;
+      if (defer && cfree[k]) cs[k] = a.vcol[p * 5 * (int64_t)vcs + col[k]];
       if (lazy && cfree[k]) {
         cs[k] = vcr[col[k]];
         cA[k] = __hiloint2double(__float_as_int(vcr[2 * vcs + col[k]]),
@@ -1401,7 +1407,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       nmax[k] = (VT)(-INFINITY); ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
-      scale[k] = !lazy && cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
+      scale[k] = !lazy && !defer && cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
       inv[k] = (VT)1;
       if constexpr (sizeof(VT) == 4) inv[k] = scale[k] ? 1.0f / total[k] : 1.0f;
     }
@@ -1486,11 +1492,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
         in.total[k] = total[k]; in.inv[k] = inv[k];
         all_scale &= scale[k] || !cfree[k];
       }
-      const int smode = (kLazy && lazy) ? 0 : (__all_sync(FULL, all_scale) ? 1 : 2);
+      const int smode = ((kLazy && lazy) || defer) ? 0 : (__all_sync(FULL, all_scale) ? 1 : 2);
       const ColOut<VT, CPL> so = stats_pass<VT, G, CPL>(tile, n, in, smode);
 #pragma unroll
       for (int k = 0; k < CPL; ++k) { nmax[k] = so.m[k]; ncnt[k] = so.c[k]; nrow[k] = so.r[k]; }
-    } else if (!lazy) {
+    } else if (!lazy && !defer) {
       // normalisation only (no aggregation): batches of 16 rows, loads first
       constexpr int RB = 16;
       int r = 0;
@@ -1522,6 +1528,18 @@ step_kernel(const __grid_constant__ StepArgs a) {
           if (!do_vel) sK[k] = cs[k];
           sc.sS[col[k]] = sK[k];
         }
+      }
+    }
+    if (defer) {
+      // deferred normalisation: s' = 1 / sum |lin| for a normalised live
+      // column, 1 otherwise (raw mode, zero column); stored in vcol row 0
+      float* vs = a.vcol + p * 5 * (int64_t)vcs;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (!cfree[k]) continue;
+        sK[k] = !do_vel ? cs[k] : ((a.normalize && total[k] > (VT)0) ? 1.0f / (float)total[k] : 1.0f);
+        sc.sS[col[k]] = sK[k];
+        if (do_vel && store_v) vs[col[k]] = sK[k];
       }
     }
     if (do_agg) {
@@ -1955,7 +1973,10 @@ step_kernel(const __grid_constant__ StepArgs a) {
               for (int j = 0; j < CPL; ++j) {
                 const int r = tid + j * NT;
                 if (r >= n || r == zc || !rf.has(r)) continue;
-                const uint64_t key = nonz_key(tile[r * n + c], sc.sS[c], false);
+                // ordered by the stored value (the column scale is positive
+                // and u * s is exact in double, so the order and the ties
+                // are those of v); nmax keeps the stored value
+                const uint64_t key = nonz_key(tile[r * n + c], 1.0f, false);
                 if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
                 else if (key == rb.key) ++rb.cnt;
               }
@@ -1965,8 +1986,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 if (col[k] == c) {
                   ncnt[k] = rr.cnt;
                   nrow[k] = rr.cnt ? rr.col : -1;
-                  nk64[k] = rr.cnt ? rr.key : 0;
                   nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
+                  nk64[k] = rr.cnt ? nonz_key(nmax[k], sc.sS[c], false) : 0;
                   recompute(k);
                 }
             }

@@ -25,6 +25,7 @@ permutations are materialised on demand by the host-view properties of
 from __future__ import annotations
 
 import math
+import os as _os
 import time
 from dataclasses import dataclass, field
 
@@ -75,7 +76,7 @@ def device_buffer_bytes(config: SolverConfig, n: int) -> int:
     p = config.num_particles
     sv = 8 if config.precision == "fp64" else 4
     vstride = -(-n * n // (16 // sv)) * (16 // sv)
-    vcol = 20 * _vcs(n) if (sv == 4 and n <= _LAZY_MAX_N) else 0
+    vcol = 20 * _vcs(n) if sv == 4 else 0
     return p * (vstride * sv + vcol + 3 * n * 2 + 2 * 8 + 16 + 1) + config.swarms * (n * 2 + 3 * 8)
 
 
@@ -149,10 +150,12 @@ class PopulationState:
             self.d_done = torch.zeros(1, dtype=torch.int32, **z)
             self.d_work = torch.zeros(1, dtype=torch.int32, **z)
             self.d_step_coef = torch.zeros((p, 2), dtype=torch.float64, **z)
-            # lazily scaled fp32 layout (one-warp kernel variants, n <= 64):
-            # V holds u, v = u * s per column; see include/qapswarm_b200.h
+            # fp32 column state: the lazily scaled layout (one-warp kernel
+            # variants, n <= 64) or, for n > 64, the deferred column scale
+            # (row 0 only); V holds u, v = u * s per column; see
+            # include/qapswarm_b200.h
             self.d_vcol = None
-            if self.v_code == _lib.F32 and n <= _LAZY_MAX_N:
+            if self.v_code == _lib.F32 and (n <= _LAZY_MAX_N or not _os.environ.get("QSB_NO_DEFER")):
                 self.d_vcol = torch.empty((p, 5, _vcs(n)), dtype=torch.float32, **z)
                 self.reset_vcol()
         except torch.OutOfMemoryError:
@@ -243,7 +246,8 @@ class PopulationState:
         the float64 value, rounded to nearest (fp32's size, fp64's exponent
         range; csrc/common.cuh wdec / wenc).  Stored-v fp32 tiles hold
         floats."""
-        return self.v_code == _lib.F32 and getattr(self, "d_vcol", None) is not None
+        return (self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N
+                and getattr(self, "d_vcol", None) is not None)
 
     def v_decode(self, u: torch.Tensor) -> torch.Tensor:
         """Stored fp32-state words -> float64 values (exact)."""
@@ -261,6 +265,8 @@ class PopulationState:
     def set_lazy_scale(self, enabled: bool):
         """Switch the fp32 state to (or from) the lazily scaled layout; V is
         materialised (u * s, rounded to the stored format) when leaving it."""
+        if self.n > _LAZY_MAX_N:
+            return      # multi-warp kernels: the deferred column scale stays
         if not enabled and self.d_vcol is not None:
             p, n = self.local_particles, self.n
             u = self.d_V[:, :n * n].view(p, n, n)

@@ -261,7 +261,7 @@ def _lazy_state_checks(st, n, normalised=True):
     return known
 
 
-@pytest.mark.parametrize("n", [7, 33, 50, 60, 64])
+@pytest.mark.parametrize("n", [7, 33, 50, 60, 64, 65, 100, 129, 200])
 @pytest.mark.parametrize("coef", [
     dict(c1=0.8, c2=0.5, c3=0.5),                                   # norm, second-target
     dict(c1=0.7, c2=1.0, c3=1.0, v_max=0.3),                        # the clamp bites
@@ -282,7 +282,9 @@ def test_fp32_lazy_layout_matrix(n, coef):
     st = qsb.init_population(cfg, inst)
     for _ in range(9):
         qsb.step(st, inst, cfg)
-    if st.d_vcol is not None:
+    perms = st.perms
+    assert (np.sort(perms, axis=1) == np.arange(n)).all(), "positions must stay permutations"
+    if st.d_vcol is not None and n <= 64:
         _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
     ost = orc.init_population(6, 20, n, inst.flow, inst.distance, seed=n)
     ost.X, ost.perms = st.X, st.perms
@@ -308,7 +310,7 @@ def test_fp32_lazy_layout_matrix(n, coef):
     cost = np.zeros(cfg.num_particles, np.int64)
     orc.cost_many(out_perm, inst.flow, inst.distance, cost)
     assert np.array_equal(cost, st.cost)
-    if st.d_vcol is not None:
+    if st.d_vcol is not None and n <= 64:
         _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
 
 
