@@ -93,6 +93,18 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else t.data_ptr()
 
 
+def wide_decode(w: torch.Tensor) -> torch.Tensor:
+    """Wide 32-bit velocity words (held in a float32 tensor) -> float64: the
+    word is the high half of the double (csrc/common.cuh wdec)."""
+    return (w.contiguous().view(torch.int32).to(torch.int64) << 32).view(torch.float64)
+
+
+def wide_encode(v: torch.Tensor) -> torch.Tensor:
+    """float64 -> wide words, rounded to nearest (csrc/common.cuh wenc)."""
+    b = (v.contiguous().view(torch.int64) + 0x80000000) >> 32
+    return b.to(torch.int32).view(torch.float32)
+
+
 class PopulationState:
     """Device-resident population (the reference's flat buffers,
     engine.py:85-124, as int16 permutations plus the velocity tensor).
@@ -251,16 +263,11 @@ class PopulationState:
 
     def v_decode(self, u: torch.Tensor) -> torch.Tensor:
         """Stored fp32-state words -> float64 values (exact)."""
-        if self.v_wide:
-            return (u.contiguous().view(torch.int32).to(torch.int64) << 32).view(torch.float64)
-        return u.double()
+        return wide_decode(u) if self.v_wide else u.double()
 
     def v_encode(self, v: torch.Tensor) -> torch.Tensor:
         """float64 values -> stored fp32-state words (rounded to nearest)."""
-        if self.v_wide:
-            b = (v.contiguous().view(torch.int64) + 0x80000000) >> 32
-            return b.to(torch.int32).view(torch.float32)
-        return v.float()
+        return wide_encode(v) if self.v_wide else v.float()
 
     def set_lazy_scale(self, enabled: bool):
         """Switch the fp32 state to (or from) the lazily scaled layout; V is

@@ -237,3 +237,29 @@ def test_ctypes_struct_layouts_match_header():
         assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
         for fname, _ in py._fields_:
             assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, f"{cname}.{fname}"
+
+
+def test_wide_velocity_words_roundtrip():
+    """The lazily scaled layout's wide words (high word of the double,
+    rounded to nearest): relative error <= 2^-21, the raw words order like
+    the values under float compares, no flush to zero over fp64's range."""
+    import torch
+    from paper_1504_05158_b200.engine import wide_decode, wide_encode
+    rng = np.random.default_rng(5)
+    mag = 2.0 ** rng.uniform(-1000, 120, 20000)
+    v = torch.from_numpy(np.where(rng.random(20000) < 0.5, -mag, mag))
+    w = wide_encode(v)
+    back = wide_decode(w)
+    rel = ((back - v).abs() / v.abs()).max().item()
+    assert rel <= 2.0 ** -21
+    assert (back != 0).all()                       # 2^-1000 survives (fp32 would flush)
+    # exactly representable values round-trip bit for bit
+    assert torch.equal(wide_decode(wide_encode(back)), back)
+    # float compares of the raw words order like the values
+    i = torch.randperm(20000)
+    j = torch.randperm(20000)
+    assert torch.equal(w[i] > w[j], back[i] > back[j])
+    assert torch.equal(w[i] == w[j], back[i] == back[j])
+    # signed zeros compare equal, as in the double domain
+    z = wide_encode(torch.tensor([0.0, -0.0], dtype=torch.float64))
+    assert z[0] == z[1]
