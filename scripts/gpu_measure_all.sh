@@ -26,7 +26,6 @@ prof() {  # name kernel-regex skip bench-args...
   ncu -i /tmp/$name.ncu-rep --page raw --csv > gpurun_out/m/${name}_raw.csv 2>/dev/null
   ncu -i /tmp/$name.ncu-rep --page details > gpurun_out/m/${name}_details.txt 2>/dev/null
   ncu -i /tmp/$name.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/m/${name}_source.csv 2>/dev/null
-  python scripts/ncu_summary.py /tmp/$name.ncu-rep $name gpurun_out/m/${name}_summary.json > /dev/null 2>&1
 }
 prof prof_step step_kernel 10 --steps 8 --warmup 5
 prof prof_step_late step_kernel 300 --steps 300 --warmup 5
