@@ -130,6 +130,15 @@ __device__ __forceinline__ float wenc(double d) {
   return __int_as_float((int)(unsigned)(b >> 32));
 }
 
+// Approximate reciprocal (MUFU.RCP, <= 1 ulp; deterministic).  Used where
+// the lazily scaled layout only needs a consistent scale, not the IEEE
+// rounded quotient (the column sums are tracked from the stored values).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // -------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -1330,7 +1330,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           // lin of a touched entry is formed in double (the pulls and the
           // inertia term can cancel), then rounded once; u' = lin / (c1 s)
           const double c1sd = a.c1 * (double)cs[k];
-          const float rc = __frcp_rn((float)c1sd);
+          const float rc = rcp_approx((float)c1sd);   // c1 s in [2^-120, 2^120]
           // statistics over the rows other than zp (the previous step's z row)
           float M = cM[k];
           int cnt = cCR[k] >> 16, R = (cCR[k] >> 8) & 0xff;
@@ -1358,14 +1358,9 @@ step_kernel(const __grid_constant__ StepArgs a) {
             else if (u == M) { if (u2 < M && (--cnt == 0 || R == r)) bad = true; }
             else if (u2 == M) { ++cnt; R = min(R, r); }
           };
-          // the <= 3 touched rows in this order (x, pl, pg), one copy of upd
-#pragma unroll 1
-          for (int j = 0; j < 3; ++j) {
-            const int r = j == 0 ? xr : (j == 1 ? lr : gr);
-            const double off = j == 0 ? offx : (j == 1 ? offl : c3r3);
-            const bool go = j == 0 ? offx != 0.0 : (j == 1 ? lr != xr : (gr != xr && gr != lr));
-            if (go) upd(r, off);
-          }
+          if (offx != 0.0) upd(xr, offx);
+          if (lr != xr) upd(lr, offl);
+          if (gr != xr && gr != lr) upd(gr, c3r3);
           if (xr != zp) {
             // the excluded row moves from zp to this step's z row xr
             const float uo = colp[zp * n];
@@ -1478,7 +1473,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
         // column: no normalisation
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-          sK[k] = (a.normalize && cA[k] > 0.0) ? __frcp_rn((float)cA[k]) : (incr ? total[k] : 1.0f);
+          sK[k] = (a.normalize && cA[k] > 0.0) ? rcp_approx((float)cA[k]) : (incr ? total[k] : 1.0f);
         stats_done = true;
       }
     }
