@@ -802,12 +802,18 @@ struct VelIn {
   float cs[CPL];
 };
 template <int CPL>
-struct VelOut { float total[CPL]; };
+struct VelOut {
+  float total[CPL];
+  // with `stats` (multi-warp, deferred normalisation): max / tie count /
+  // first row of the new column over its non-z rows
+  float m[CPL];
+  int c[CPL], r[CPL];
+};
 
 template <int G, int CPL>
 __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn<CPL> in, double c1,
                                                  double c2r2, double c3r3, double vmax, int v_bounded,
-                                                 bool wide) {
+                                                 bool wide, bool stats = false) {
   // wide (the lazily scaled layout): the tile holds wide words (wdec /
   // wenc), decoded to double, scaled and clamped in double, re-encoded;
   // otherwise plain floats in float arithmetic
@@ -820,6 +826,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   for (int k = 0; k < CPL; ++k) {
     col[k] = in.col[k]; zr[k] = in.zr[k]; plr[k] = in.plr[k]; pgr[k] = in.pgr[k];
     cfree[k] = in.cfree[k]; cs[k] = in.cs[k]; o.total[k] = 0.0f;
+    o.m[k] = -INFINITY; o.c[k] = 0; o.r[k] = -1;
   }
   // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
   // x / pl / pg are patched afterwards (sum order is not significant
@@ -922,6 +929,13 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
     // batches of 8 rows, loads first: with the tile in global memory (GT)
     // the column walk is latency-bound unless many loads are in flight
     constexpr int RB = G >= 8 ? 16 : 8;   // deeper for the global-memory tiles (n > 128)
+    // column statistics of the written values (stats): rows ascend, so a
+    // strict > keeps the first row of the maximum
+    auto track = [&](float w, int row, int k) {
+      if (row == zr[k]) return;
+      if (w > o.m[k]) { o.m[k] = w; o.c[k] = 1; o.r[k] = row; }
+      else if (w == o.m[k]) ++o.c[k];
+    };
     int r = 0;
     for (; r + RB <= n; r += RB) {
 #pragma unroll
@@ -934,8 +948,10 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
           float mag;
-          cell[b * n] = step1(x[b], k, c1k[k], c1kd[k], mag);
+          const float w = step1(x[b], k, c1k[k], c1kd[k], mag);
+          cell[b * n] = w;
           if (b & 1) tot2[k] += mag; else tot[k] += mag;
+          if (stats) track(w, r + b, k);
         }
       }
     }
@@ -945,8 +961,10 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
         if (!cfree[k]) continue;
         float* cell = reinterpret_cast<float*>(tile) + r * n + col[k];
         float mag;
-        cell[0] = step1(cell[0], k, c1k[k], c1kd[k], mag);
+        const float w = step1(cell[0], k, c1k[k], c1kd[k], mag);
+        cell[0] = w;
         tot[k] += mag;
+        if (stats) track(w, r, k);
       }
     }
   }
@@ -957,13 +975,14 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
     if (!cfree[k]) continue;
     const int xr = zr[k], lr = plr[k], gr = pgr[k];
     float* colp = reinterpret_cast<float*>(tile) + col[k];
+    bool bad = false;
     auto fix = [&](int r, float v0) {
       const float d2 = (float)((r == lr) - (r == xr));
       const float d3 = (float)((r == gr) - (r == xr));
       // the loop's value for this row (its magnitude is in the sum), then
       // the exact one; in double: the pulls and the inertia term can cancel
       float gmag;
-      (void)step1(v0, k, c1k[k], c1kd[k], gmag);
+      const float g = step1(v0, k, c1k[k], c1kd[k], gmag);
       const double vd = WF ? wdec(v0) : (double)v0;
       const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * (vd * (double)cs[k])));
       if (WF) {
@@ -974,12 +993,33 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
         const float sp = (float)fmin(fmax(l, -vmax), vmax);
         colp[r * n] = sp;
         tot[k] += fabsf(sp) - gmag;
+        if (stats && r != xr) {
+          // the loop counted g for this row; replace it by sp
+          float& M = o.m[k];
+          int& cnt = o.c[k];
+          int& R = o.r[k];
+          if (sp > M) { M = sp; cnt = 1; R = r; }
+          else if (g == M) { if (sp < M && (--cnt == 0 || R == r)) bad = true; }
+          else if (sp == M) { ++cnt; R = min(R, r); }
+        }
       }
     };
     fix(xr, vx[k]);
     if (lr != xr) fix(lr, vl[k]);
     if (gr != xr && gr != lr) fix(gr, vg[k]);
     o.total[k] = tot[k];
+    if (stats && bad) {
+      // a touched row held the maximum and fell below it: rescan the column
+      float M = -INFINITY;
+      int cnt = 0, R = -1;
+      for (int rr = 0; rr < n; ++rr) {
+        if (rr == xr) continue;
+        const float w = colp[rr * n];
+        if (w > M) { M = w; cnt = 1; R = rr; }
+        else if (w == M) ++cnt;
+      }
+      o.m[k] = M; o.c[k] = cnt; o.r[k] = R;
+    }
   }
   return o;
 }
@@ -1265,6 +1305,9 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // Row-outer loops over the CPL owned columns: every column still sums in
     // row order (the reference's order), and the lanes share loop overhead.
     VT total[CPL];
+    float vnm[CPL];          // column statistics from the velocity walk (deferred
+    int vnc[CPL], vnr[CPL];  // normalisation, multi-warp fp32)
+    bool vstats = false;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) total[k] = (VT)0;
     if (do_vel) {
@@ -1385,9 +1428,17 @@ step_kernel(const __grid_constant__ StepArgs a) {
           vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k];
         }
         const VelOut<CPL> vo = vel_full_f32<G, CPL>(reinterpret_cast<float*>(tile), n, vi, a.c1, c2r2,
-                                                    c3r3, a.vmax, a.v_bounded, wide);
+                                                    c3r3, a.vmax, a.v_bounded, wide, GT && defer && do_agg);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) total[k] = (VT)vo.total[k];
+        if (GT && defer && do_agg) {
+          // deferred normalisation keeps the written values: their column
+          // statistics came out of the velocity walk (no second pass over a
+          // global-memory tile; smem tiles keep the two-chain stats pass)
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) { vnm[k] = vo.m[k]; vnc[k] = vo.c[k]; vnr[k] = vo.r[k]; }
+          vstats = true;
+        }
       }
     }
 
@@ -1414,6 +1465,15 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) sK[k] = 1.0f;
     bool stats_done = false;
+    if constexpr (sizeof(VT) == 4 && G > 1) {
+      if (vstats) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          nmax[k] = vnm[k]; ncnt[k] = cfree[k] ? vnc[k] : 0; nrow[k] = ncnt[k] ? vnr[k] : -1;
+        }
+        stats_done = true;
+      }
+    }
     if constexpr (kLazy) {
       if (lazy && do_vel) {
         // incremental step: the non-z statistics were carried through the
