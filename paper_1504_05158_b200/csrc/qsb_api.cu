@@ -220,7 +220,6 @@ static int launch_twoopt_tc(TwoOptArgs t, cudaStream_t s) {
   const int by_smem = (int)((smem_optin() + 1024) / (smem + stat + 1024));
   int bps = by_regs < by_smem ? by_regs : by_smem;
   if (bps > 512 / g.tcols) bps = 512 / g.tcols;
-  if (getenv("QSB_DEBUG")) fprintf(stderr, "twoopt_tc n=%d smem=%zu bps=%d (regs %d smem %d)\n", t.n, smem, bps, by_regs, by_smem);
   if (bps < 1) bps = 1;
   const int64_t cap = (int64_t)num_sms() * bps;
   const int grid = (int)(t.P < cap ? t.P : cap);

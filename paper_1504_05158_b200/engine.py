@@ -167,6 +167,8 @@ class PopulationState:
             # (row 0 only); V holds u, v = u * s per column; see
             # include/qapswarm_b200.h
             self.d_vcol = None
+            # (QSB_NO_DEFER=1: multi-warp fp32 tiles normalised in place
+            # instead, the pre-deferral layout, for A/B measurements)
             if self.v_code == _lib.F32 and (n <= _LAZY_MAX_N or not _os.environ.get("QSB_NO_DEFER")):
                 self.d_vcol = torch.empty((p, 5, _vcs(n)), dtype=torch.float32, **z)
                 self.reset_vcol()
