@@ -44,7 +44,10 @@ def parse():
     ap.add_argument("--swarms", type=int, default=SWARMS)
     ap.add_argument("--swarm-size", type=int, default=SWARM_SIZE)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=-1,
+                    help="steps of the end-to-end (public API) measurement; default = --steps, "
+                         "run on a fresh population over the same iterations as the device-timed "
+                         "window (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--velocity-only", action="store_true",
@@ -386,9 +389,16 @@ def main():
 
     # ---- end to end through the public API: step() + D2H of the step's
     # per-particle costs and best record, synchronised every step
-    e2e_steps = args.e2e_steps if flags is None else 0
+    e2e_steps = (args.steps if args.e2e_steps < 0 else args.e2e_steps) if flags is None else 0
     e2e = None
     if e2e_steps:
+        # a fresh population, warmed up like the device-timed run, so the
+        # end-to-end window covers the same iterations (W+1 .. W+K)
+        del state
+        torch.cuda.empty_cache()
+        state = qsb.init_population(cfg, inst, device=dev, swarm_range=(lo, hi))
+        for _ in range(args.warmup):
+            qsb.step(state, inst, cfg, exchange=exchange)
         # double-buffered pinned results: the host reads step i's costs while
         # step i+1 runs (every step's result still crosses to the host)
         host_cost = [torch.empty(state.local_particles, dtype=state.d_cost.dtype, pin_memory=True)
@@ -423,7 +433,8 @@ def main():
                "steps": e2e_steps,
                "how": "public step() per iteration + D2H of that iteration's per-particle cost "
                       "vector and best cost into pinned memory, read on the host one step behind "
-                      "(double-buffered), wall clock, max over ranks; the population stays "
+                      "(double-buffered), wall clock, max over ranks, on a fresh population over "
+                      "the same iterations as the device-timed window; the population stays "
                       "resident (the random streams are generated in-kernel, so an iteration has "
                       "no host inputs)"}
 
