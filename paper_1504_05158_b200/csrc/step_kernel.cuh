@@ -1027,13 +1027,13 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
 // Loads of particle pp into the group's staging area: one bulk copy of the
 // tile (and, lazily scaled, its column state) on the group's mbarrier, and
 // cp.async copies of the perm / pl_perm / pg_perm rows, (c2 r2, c3 r3) and
-// (cost, pl_cost) into buffer `buf`.  Out of line: it has two call sites
-// (the first particle and the prefetch after the aggregation), and one copy
-// keeps the per-particle path smaller in the instruction cache.
+// (cost, pl_cost) into buffer `buf`.  Inlined at its two call sites (the
+// first particle and the prefetch after the aggregation): an out-of-line
+// copy saved 7 KB of SASS but cost 2-3 % (call overhead, register saves).
 enum LoadFlags : int { L_LAZY = 1, L_PERM = 2, L_COST = 4, L_PL = 8, L_VEL = 16 };
 
 template <typename K, typename VT>
-__device__ __noinline__ void issue_particle_load(const StepArgs* ap, int64_t pp, int buf, int tid,
+__device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t pp, int buf, int tid,
                                                  int lane, VT* tile, unsigned char* stg, uint64_t* bar,
                                                  uint32_t tile_bytes, uint32_t col_bytes, int lf,
                                                  double inv_s) {
