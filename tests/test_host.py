@@ -263,3 +263,23 @@ def test_wide_velocity_words_roundtrip():
     # signed zeros compare equal, as in the double domain
     z = wide_encode(torch.tensor([0.0, -0.0], dtype=torch.float64))
     assert z[0] == z[1]
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` runs on the host cores alone (the oracle
+    port; no GPU) and prints one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--n", "12", "--swarms", "80"],
+                         capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
