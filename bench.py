@@ -32,6 +32,7 @@ METRIC = "particle-iterations/sec (QAP n=50, 80k particles)"   # the headline (c
 UNIT = "particle-iterations/s"
 N_DEFAULT, SWARMS, SWARM_SIZE = 50, 800, 100
 PERIOD, FACTOR, SEED = 10, 0.33, 1
+L2_BYTES = 126 << 20     # B200 L2
 
 
 def parse():
@@ -309,11 +310,21 @@ def main():
     import paper_1504_05158_b200 as qsb
     from paper_1504_05158_b200 import engine, shard
 
+    # functional check of the multi-rank path on a one-GPU box (not a
+    # measurement): QSB_BENCH_BACKEND=gloo QSB_BENCH_SAME_DEVICE=1 puts every
+    # rank on cuda:0 with host-level collectives (no kernel waits on another
+    # rank); the driver's runs use NCCL, one GPU per rank
+    backend = os.environ.get("QSB_BENCH_BACKEND", "nccl")
+    if os.environ.get("QSB_BENCH_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     inst = qsb.taillard_uniform(args.n)
     cfg = config(args)
     lo, hi = shard.swarm_range(cfg.swarms, world, rank)
@@ -357,15 +368,34 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # inputs smaller than L2: flush it (write a 256 MB buffer) before every
+    # timed step and time the steps one by one, outside the flushes
+    vbytes = state.local_particles * state.vstride * (4 if cfg.precision == "fp32" else 8)
+    use_graph = args.graph and world == 1 and flags is None
+    flush_l2 = vbytes < 2 * L2_BYTES and not use_graph
+    step_ms = None
     t_start.record(stream)
-    if args.graph and world == 1 and flags is None:
+    if use_graph:
         timer.active = False
         qsb.step_many(state, inst, cfg, args.steps)
+    elif flush_l2:
+        scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        pairs = []
+        for _ in range(args.steps):
+            scratch.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one_step()
+            e1.record(stream)
+            pairs.append((e0, e1))
     else:
         for _ in range(args.steps):
             one_step()
     t_end.record(stream)
     torch.cuda.synchronize()
+    if flush_l2:
+        step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     if world > 1:
         dist.barrier()
     if args.graph and world == 1 and flags is None:
@@ -375,7 +405,7 @@ def main():
         torch.cuda.synchronize()
     timer.active = False
     clock_rec = clocks.stop() if clocks else None
-    ms = t_start.elapsed_time(t_end)
+    ms = step_ms if step_ms is not None else t_start.elapsed_time(t_end)
     launches = state.launches - launches0
     if args.graph and world == 1 and flags is None:
         launches //= 2          # the eager roofline window doubled the count
@@ -496,7 +526,14 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if cfg.precision == "fp32" else "f64", "data": "synthetic",
-                "config": workload(args, world), "roofline": roofline, "cpu_baseline": cpu,
+                "config": dict(workload(args, world), l2=(
+                    f"velocity state {vbytes / 1e6:.0f} MB per GPU "
+                    + ("< 2 x L2: L2 flushed (256 MB write) before every timed step, steps timed "
+                       "one by one" if flush_l2 else
+                       "< 2 x L2, CUDA-graph replay without flushes (launch-latency bound)"
+                       if use_graph and vbytes < 2 * L2_BYTES else
+                       "> 2 x L2 (126 MB): inputs larger than L2"))),
+                "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clock_rec,
                 "roofline_twoopt": roofline2,
                 "best_cost": best.cost if best else state.best_cost}
