@@ -1499,23 +1499,29 @@ step_kernel(const __grid_constant__ StepArgs a) {
             const int c = src + k * 32;
             const int zc = __shfl_sync(FULL, zr[k], src);
             if (__shfl_sync(FULL, cCR[k], src) < 0) QSB_COUNT(10, 1);
-            unsigned km = 0, kc = 0, kr = INT_MAX;
+            unsigned kj[CPL];
+            unsigned km = 0;
             double sum = 0.0;
 #pragma unroll
             for (int j = 0; j < CPL; ++j) {
               const int r = lane + j * 32;
+              kj[j] = 0u;
               if (r >= n) continue;
               const float u = (float)tile[r * n + c];   // wide word
               sum += fabs(wdec(u));
               if (r == zc) continue;
-              const unsigned key = okey32(__fadd_rn(u, 0.0f));
-              if (key > km) { km = key; kc = 1; kr = r; }
-              else if (key == km) ++kc;
+              kj[j] = okey32(__fadd_rn(u, 0.0f));
+              km = max(km, kj[j]);
             }
+            // the maximum by one reduction, its rows by ballots
             const unsigned M = __reduce_max_sync(FULL, km);
-            const bool match = km == M && kc > 0;
-            const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
-            const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
+            unsigned tot = 0, rr = INT_MAX;
+#pragma unroll
+            for (int j = CPL - 1; j >= 0; --j) {
+              const unsigned b = __ballot_sync(FULL, M != 0u && kj[j] == M);
+              tot += __popc(b);
+              if (b) rr = j * 32 + __ffs(b) - 1;
+            }
 #pragma unroll
             for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
             if (lane == src) {
@@ -1971,19 +1977,26 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 const int zc = __shfl_sync(FULL, zr[k], src);
                 if constexpr (sizeof(VT) == 4) {
                   // fp32: one 32-bit key per cell, three warp reductions
-                  unsigned km = 0, kc = 0, kr = INT_MAX;
+                  // one key per cell (lane = row, + 32 j), the maximum by one
+                  // reduction, its rows by ballots: count = popc, first row
+                  // = lowest set bit in row order
+                  unsigned kj[CPL];
+                  unsigned km = 0;
 #pragma unroll
                   for (int j = 0; j < CPL; ++j) {
                     const int r = lane + j * 32;
-                    if (r >= n || r == zc || !rf.has(r)) continue;
-                    const unsigned key = okey32(__fadd_rn((float)tile[r * n + c], 0.0f));
-                    if (key > km) { km = key; kc = 1; kr = r; }
-                    else if (key == km) ++kc;
+                    kj[j] = (r >= n || r == zc || !rf.has(r)) ? 0u
+                            : okey32(__fadd_rn((float)tile[r * n + c], 0.0f));
+                    km = max(km, kj[j]);
                   }
                   const unsigned M = __reduce_max_sync(FULL, km);
-                  const bool match = km == M && kc > 0;
-                  const unsigned tot = __reduce_add_sync(FULL, match ? kc : 0u);
-                  const unsigned rr = __reduce_min_sync(FULL, match ? kr : (unsigned)INT_MAX);
+                  unsigned tot = 0, rr = INT_MAX;
+#pragma unroll
+                  for (int j = CPL - 1; j >= 0; --j) {
+                    const unsigned b = __ballot_sync(FULL, M != 0u && kj[j] == M);
+                    tot += __popc(b);
+                    if (b) rr = j * 32 + __ffs(b) - 1;
+                  }
                   if (lane == src) {
                     ncnt[k] = (int)tot;
                     nrow[k] = tot ? (int)rr : -1;
