@@ -98,12 +98,13 @@ typedef struct qsb_state {
   /* Lazily scaled fp32 layout (optional; NULL = V holds v itself).  When set
    * (v_dtype QSB_F32, n <= 64), V holds u and the velocity is v = u * s
    * per column; vcol is (P, 5, vcs) 32-bit words with vcs = n rounded up to
-   * a multiple of 4: row 0 the column scale s (f32), rows 1-2 the low / high
+   * a multiple of 4: row 0 the column scale s (a wide word, like V; 1.0 is
+   * the bit pattern 0x3FF00000), rows 1-2 the low / high
    * words of the f64 sum of |u| over the column, row 3 the maximum of u over
    * the rows other than zp (a wide word, NaN = unknown), row 4 (int32) count << 16 |
    * first row << 8 | zp, zp being the z row (the position) of the step that
-   * wrote them.  Set row 0 to 1 and row 3 to NaN whenever V is written from
-   * outside the step.  For n > 64 (multi-warp kernels) only row 0 is used:
+   * wrote them.  Set row 0 to 1.0 (0x3FF00000) and row 3 to NaN whenever V is
+   * written from outside the step.  For n > 64 (multi-warp kernels) only row 0 is used:
    * the deferred column normalisation, V holds the unnormalised velocity u
    * (floats) and v = u * s. */
   float* vcol;

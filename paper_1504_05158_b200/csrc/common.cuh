@@ -139,6 +139,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+// Approximate reciprocal of a positive normal double (mantissa by MUFU.RCP,
+// exponent by integer arithmetic; deterministic, relative error ~2^-23):
+// the lazily scaled layout's wide column scales span the double range.
+__device__ __forceinline__ double drcp_approx(double x) {
+  const long long b = __double_as_longlong(x);
+  const long long e = ((b >> 52) & 0x7ff) - 1023;
+  const double m = __longlong_as_double((b & 0x000fffffffffffffLL) | (1023LL << 52));   // [1, 2)
+  const double r = (double)rcp_approx((float)m);                                        // (0.5, 1]
+  return __longlong_as_double(__double_as_longlong(r) - (e << 52));
+}
+
 // -------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -277,7 +277,7 @@ __device__ __forceinline__ int group_min_int(int x, Scratch& sc, int& ipar, int 
 template <typename VT>
 __device__ __forceinline__ double vval(VT u, float s, bool wide) {
   if constexpr (sizeof(VT) == 8) return u;
-  else return (wide ? wdec(u) : (double)u) * (double)s;
+  else return wide ? wdec(u) * wdec(s) : (double)u * (double)s;   // wide: the scale is a wide word too
 }
 template <typename VT>
 __device__ __forceinline__ uint64_t nonz_key(VT v, float s, bool wide) {   // key of m = 0.0 + v
@@ -800,6 +800,7 @@ struct VelIn {
   int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
   bool cfree[CPL];
   float cs[CPL];
+  double csd[CPL];   // the column scale as a double (lazily scaled layout: decoded wide word)
 };
 template <int CPL>
 struct VelOut {
@@ -822,10 +823,11 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   int col[CPL], zr[CPL], plr[CPL], pgr[CPL];
   bool cfree[CPL];
   float cs[CPL];
+  double csd[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
     col[k] = in.col[k]; zr[k] = in.zr[k]; plr[k] = in.plr[k]; pgr[k] = in.pgr[k];
-    cfree[k] = in.cfree[k]; cs[k] = in.cs[k]; o.total[k] = 0.0f;
+    cfree[k] = in.cfree[k]; cs[k] = in.cs[k]; csd[k] = in.csd[k]; o.total[k] = 0.0f;
     o.m[k] = -INFINITY; o.c[k] = 0; o.r[k] = -1;
   }
   // throughput mode: bulk rows are c1*v; the <= 3 rows touched by
@@ -837,7 +839,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
   float c1k[CPL];
   double c1kd[CPL];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) { c1k[k] = c1f * cs[k]; c1kd[k] = (double)c1f * (double)cs[k]; }
+  for (int k = 0; k < CPL; ++k) { c1k[k] = c1f * cs[k]; c1kd[k] = (double)c1f * csd[k]; }
   float vx[CPL], vl[CPL], vg[CPL], tot[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
@@ -984,7 +986,7 @@ __device__ __noinline__ VelOut<CPL> vel_full_f32(float* tile, int n, const VelIn
       float gmag;
       const float g = step1(v0, k, c1k[k], c1kd[k], gmag);
       const double vd = WF ? wdec(v0) : (double)v0;
-      const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * (vd * (double)cs[k])));
+      const double l = fma(c3r3, (double)d3, fma(c2r2, (double)d2, c1 * (vd * csd[k])));
       if (WF) {
         const double sp = fmin(fmax(l, -vmax), vmax);
         colp[r * n] = wenc(sp);
@@ -1246,6 +1248,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // and the max / tie count / first row of u over the rows other than the
     // z row zp of the step that wrote them (M = NaN: not known)
     float cs[CPL], cM[CPL];
+    double csd[CPL];   // the column scale (lazily scaled layout: a wide word, decoded)
     double cA[CPL];
     int cCR[CPL];
     float* vcp = lazy ? a.vcol + p * 5 * (int64_t)vcs : nullptr;
@@ -1261,6 +1264,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
         cM[k] = vcr[3 * vcs + col[k]];
         cCR[k] = __float_as_int(vcr[4 * vcs + col[k]]);
       }
+      csd[k] = lazy ? wdec(cs[k]) : (double)cs[k];
     }
     double c2r2 = 0.0, c3r3 = 0.0;
     if (do_vel) {
@@ -1288,9 +1292,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
-        const float c1s = c1f * cs[k];
-        ok &= cM[k] == cM[k] && cs[k] >= 0x1p-110f && cs[k] <= 0x1p110f && c1s >= 0x1p-120f &&
-              c1s <= 0x1p120f && c1s >= lb * 0x1p-125f;
+        // wide scale and words: the range only has to keep u' = lin / (c1 s)
+        // and the products u * s inside the double exponent range
+        const double c1s = a.c1 * csd[k];
+        ok &= cM[k] == cM[k] && csd[k] >= 0x1p-900 && csd[k] <= 0x1p900 && c1s >= 0x1p-900 &&
+              c1s <= 0x1p900 && c1s >= (double)lb * 0x1p-900;
       }
       incr = __all_sync(FULL, ok);
       if (!incr) QSB_COUNT(8, 1);
@@ -1305,6 +1311,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // Row-outer loops over the CPL owned columns: every column still sums in
     // row order (the reference's order), and the lanes share loop overhead.
     VT total[CPL];
+    double c1sdk[CPL];   // incremental lazy step: the column factor c1 * s
     float vnm[CPL];          // column statistics from the velocity walk (deferred
     int vnc[CPL], vnr[CPL];  // normalisation, multi-warp fp32)
     bool vstats = false;
@@ -1372,8 +1379,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
           const int xr = zr[k], lr = plr[k], gr = pgr[k];
           // lin of a touched entry is formed in double (the pulls and the
           // inertia term can cancel), then rounded once; u' = lin / (c1 s)
-          const double c1sd = a.c1 * (double)cs[k];
-          const float rc = rcp_approx((float)c1sd);   // c1 s in [2^-120, 2^120]
+          const double c1sd = a.c1 * csd[k];
+          const double rcd = drcp_approx(c1sd);       // c1 s in [2^-900, 2^900]
           // statistics over the rows other than zp (the previous step's z row)
           float M = cM[k];
           int cnt = cCR[k] >> 16, R = (cCR[k] >> 8) & 0xff;
@@ -1391,7 +1398,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
             const float u = colp[r * n];             // wide word
             const double ud = wdec(u);
             const float lin = fminf(fmaxf((float)fma(c1sd, ud, off), -vm), vm);
-            const double u2d = (double)lin * (double)rc;
+            const double u2d = (double)lin * rcd;
             const float u2 = wenc(u2d);
             colp[r * n] = u2;
             if (store_v) gcol[r * n] = u2;
@@ -1418,6 +1425,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           cM[k] = M;
           cCR[k] = bad ? -1 : ((cnt << 16) | (R << 8) | xr);
           total[k] = (float)c1sd;   // incremental mode: total carries the column factor c1 * s
+          c1sdk[k] = c1sd;
         }
         fence_proxy_async_smem();   // generic tile writes before the next bulk load
       } else {
@@ -1425,7 +1433,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           vi.col[k] = col[k]; vi.zr[k] = zr[k]; vi.plr[k] = plr[k]; vi.pgr[k] = pgr[k];
-          vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k];
+          vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k]; vi.csd[k] = csd[k];
         }
         const VelOut<CPL> vo = vel_full_f32<G, CPL>(reinterpret_cast<float*>(tile), n, vi, a.c1, c2r2,
                                                     c3r3, a.vmax, a.v_bounded, wide, GT && defer && do_agg);
@@ -1539,7 +1547,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
         // column: no normalisation
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-          sK[k] = (a.normalize && cA[k] > 0.0) ? rcp_approx((float)cA[k]) : (incr ? total[k] : 1.0f);
+          // the new scale as a wide word (double range, so no renormalising pass)
+          sK[k] = wenc((a.normalize && cA[k] > 0.0) ? drcp_approx(cA[k]) : (incr ? c1sdk[k] : 1.0));
         stats_done = true;
       }
     }

@@ -249,7 +249,10 @@ class PopulationState:
         outside the step: scale 1, statistics unknown (the next step runs
         the full pass)."""
         if self.d_vcol is not None:
-            self.d_vcol[:, 0].fill_(1.0)
+            if self.v_wide:
+                self.d_vcol[:, 0].view(torch.int32).fill_(0x3FF00000)   # the wide word of 1.0
+            else:
+                self.d_vcol[:, 0].fill_(1.0)
             self.d_vcol[:, 1:3].zero_()
             self.d_vcol[:, 3].fill_(float("nan"))
             self.d_vcol[:, 4].zero_()
@@ -279,7 +282,7 @@ class PopulationState:
         if not enabled and self.d_vcol is not None:
             p, n = self.local_particles, self.n
             u = self.d_V[:, :n * n].view(p, n, n)
-            v = self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)
+            v = self.v_decode(u) * self.v_decode(self.d_vcol[:, 0, :n]).unsqueeze(1)
             self.d_vcol = None                # stored-v: plain floats
             u.copy_(v.float())
         elif enabled and self.d_vcol is None and self.v_code == _lib.F32 and self.n <= _LAZY_MAX_N:
@@ -299,7 +302,7 @@ class PopulationState:
         p, n, nn = self.local_particles, self.n, self.n * self.n
         u = self.d_V[:, :nn].view(p, n, n)
         if self.d_vcol is not None:
-            return (self.v_decode(u) * self.d_vcol[:, 0, :n].double().unsqueeze(1)).cpu().numpy()
+            return (self.v_decode(u) * self.v_decode(self.d_vcol[:, 0, :n]).unsqueeze(1)).cpu().numpy()
         return u.cpu().numpy()
 
     @property

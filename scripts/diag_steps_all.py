@@ -5,9 +5,10 @@ import torch
 import paper_1504_05158_b200 as qsb
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 500
 mig = float(sys.argv[2]) if len(sys.argv) > 2 else 0.33
+period = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 inst = qsb.taillard_uniform(50)
 cfg = qsb.SolverConfig(swarms=800, swarm_size=100, seed=1, precision="fp32", init="device",
-                       migration_factor=mig, migration_period=10,
+                       migration_factor=mig, migration_period=period,
                        coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
 st = qsb.init_population(cfg, inst)
 class T:

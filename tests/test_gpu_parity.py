@@ -238,7 +238,7 @@ def _lazy_state_checks(st, n, normalised=True):
     p = st.local_particles
     u = st.v_decode(st.d_V[:, :n * n].view(p, n, n)).cpu().numpy()   # stored words -> values
     vc = st.d_vcol.cpu()
-    s = vc[:, 0, :n].double().numpy()
+    s = st.v_decode(vc[:, 0, :n]).numpy()                        # wide word: the column scale
     words = vc.view(torch.int32).numpy().astype(np.int64) & 0xFFFFFFFF
     A = ((words[:, 2, :n] << 32) | words[:, 1, :n]).view(np.float64)
     known = ~torch.isnan(vc[:, 3, :n]).numpy()          # NaN word: statistics unknown
@@ -359,7 +359,7 @@ def test_fp32_lazy_column_state_invariants(name, steps, c1, golden_instances):
     n, p = inst.n, st.local_particles
     u = st.v_decode(st.d_V[:, :n * n].view(p, n, n)).cpu().numpy()   # stored words -> values
     vc = st.d_vcol.cpu()
-    s = vc[:, 0, :n].double().numpy()
+    s = st.v_decode(vc[:, 0, :n]).numpy()                        # wide word: the column scale
     words = vc.view(torch.int32).numpy().astype(np.int64) & 0xFFFFFFFF
     A = ((words[:, 2, :n] << 32) | words[:, 1, :n]).view(np.float64)
     known = ~torch.isnan(vc[:, 3, :n]).numpy()          # NaN word: statistics unknown
