@@ -19,7 +19,7 @@ names = ["particles", "normal_rounds", "bulk_steps", "bulk_cells", "tie_rounds",
 L.qsb_debug_counters(buf)
 for t in range(1, 401):
     qsb.step(st, inst, cfg)
-    if t in (1, 10, 50, 100, 200, 300, 400):
+    if t in (1, 10, 50, 100, 150, 200, 300, 400):
         torch.cuda.synchronize()
         L.qsb_debug_counters(buf)
         P = buf[0]
