@@ -57,6 +57,8 @@ __device__ __forceinline__ CT ct_max() {
 // global best, which the last-arriving block applies (strict <, first index).
 template <typename CT, int WPB>
 __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
+  pdl_wait();     // costs / improved flags of the step kernel
+  pdl_launch();   // the next step's coef_kernel waits on this grid anyway
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
   const CT* cost = reinterpret_cast<const CT*>(a.cost);
@@ -65,16 +67,30 @@ __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
     CT bi = ct_max<CT>(), ba = ct_max<CT>();
     int64_t ii = INT64_MAX, ia = INT64_MAX;
     const int64_t lo = k * a.S;
-    for (int64_t q = lane; q < a.S; q += 32) {
-      const int64_t i = lo + q;
-      const CT c = cost[i];
-      if (lex_less(c, i, ba, ia)) { ba = c; ia = i; }
-      if (a.improved[i] && lex_less(c, i, bi, ii)) { bi = c; ii = i; }
+    CT* pgc = reinterpret_cast<CT*>(a.pg_cost);
+    const CT pg_old = pgc[k];
+    // four loads in flight per lane before any compare (S = 100: one batch)
+    for (int64_t q0 = 0; q0 < a.S; q0 += 128) {
+      CT cv[4];
+      bool iv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t q = q0 + lane + 32 * j;
+        cv[j] = q < a.S ? cost[lo + q] : ct_max<CT>();
+        iv[j] = q < a.S ? a.improved[lo + q] != 0 : false;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t q = q0 + lane + 32 * j;
+        if (q >= a.S) continue;
+        const int64_t i = lo + q;
+        if (lex_less(cv[j], i, ba, ia)) { ba = cv[j]; ia = i; }
+        if (iv[j] && lex_less(cv[j], i, bi, ii)) { bi = cv[j]; ii = i; }
+      }
     }
     warp_lexmin(bi, ii);
     warp_lexmin(ba, ia);
-    CT* pgc = reinterpret_cast<CT*>(a.pg_cost);
-    if (ii != INT64_MAX && bi < pgc[k]) {
+    if (ii != INT64_MAX && bi < pg_old) {
       for (int c = lane; c < n; c += 32) a.pg_perm[k * n + c] = a.perm_new[ii * n + c];
       if (lane == 0) pgc[k] = bi;
     }
@@ -306,7 +322,11 @@ __global__ void draws_kernel(uint64_t seed, uint64_t t, int64_t p0, int64_t P, i
 // the step kernel: keeps the dependent Philox chain off the step kernel's
 // per-particle critical path.
 __global__ void coef_kernel(uint64_t seed, const int64_t* t_dev, uint64_t t_host, int64_t p0,
-                            int64_t P, int n, double c2, double c3, double* out) {
+                            int64_t P, int n, double c2, double c3, double* out, unsigned* work) {
+  pdl_wait();     // t_dev is advanced by the previous step's best_kernel
+  pdl_launch();   // the step kernel may stage its constants meanwhile
+  // the step kernel's particle counter, reset here instead of by a memset
+  if (work && blockIdx.x == 0 && threadIdx.x == 0) *work = 0u;
   const uint64_t t = t_dev ? (uint64_t)(*t_dev) + 1 : t_host;
   const uint64_t word1 = stream_word(2, t);
   const uint64_t w = 2 + 2 * (uint64_t)n;

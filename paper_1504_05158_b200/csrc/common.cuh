@@ -155,6 +155,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with the
+// programmatic-stream-serialization attribute may start while the previous
+// kernel in the stream is still running; pdl_wait() blocks until that kernel
+// has finished and its writes are visible, so every PDL kernel calls it
+// before touching memory a predecessor may write.  pdl_launch() lets the
+// next PDL kernel in the stream start early.  Both are no-ops without the
+// attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
 }

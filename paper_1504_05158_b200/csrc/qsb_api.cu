@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/qapswarm_b200.h"
@@ -32,6 +33,35 @@ static int num_sms() {
     if (sms <= 0) sms = 148;
   }
   return sms;
+}
+
+// Launch with programmatic stream serialization (PDL) so the kernel's launch
+// overlaps the tail of the previous kernel in the stream; the kernel itself
+// calls pdl_wait() before reading anything.  QSB_NO_PDL=1 launches plainly
+// (A/B knob).
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("QSB_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Act>
+static int launch_pdl(void (*fn)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                      Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cuda_status(cudaLaunchKernelEx(&cfg, fn, std::forward<Act>(args)...));
 }
 
 static size_t smem_optin() {
@@ -74,8 +104,7 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   const int64_t want = (a.P + W - 1) / W;
   const int64_t cap = (int64_t)num_sms() * occ_blocks;
   const int grid = (int)(want < cap ? want : cap);
-  fn<<<grid, 32 * G * W, smem, s>>>(b);
-  return launch_status();
+  return launch_pdl(fn, grid, 32 * G * W, smem, s, b);
 }
 
 template <typename VT, typename MT, bool DRY>
@@ -363,18 +392,20 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
   a.inj_stride = inj_stride;
   a.agg_base = agg_base;
   a.coef = coef;
+  bool work_reset = false;
   if (!coef && !inj_draws && (flags & QSB_PHASE_VELOCITY) && st->step_coef && st->num_particles > 0) {
     // the step's (c2 r2, c3 r3) from a one-thread-per-particle pre-pass
     const int64_t P = st->num_particles;
     const int grid = (int)((P + 255) / 256 < 4 * num_sms() ? (P + 255) / 256 : 4 * num_sms());
-    coef_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(co->seed, st->iteration, t_host, st->particle_offset,
-                                                         P, st->n, co->c2, co->c3, st->step_coef);
-    const int rc = launch_status();
+    const int rc = launch_pdl(coef_kernel, grid, 256, 0, (cudaStream_t)stream, co->seed,
+                              (const int64_t*)st->iteration, t_host, st->particle_offset, P, st->n,
+                              co->c2, co->c3, st->step_coef, (unsigned*)st->work);
     if (rc) return rc;
     a.coef = st->step_coef;
+    work_reset = true;   // coef_kernel zeroed the particle counter
   }
   a.work = st->work;
-  if (a.work) {
+  if (a.work && !work_reset) {
     cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(unsigned int), (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_status(e);
   }
@@ -406,12 +437,10 @@ int qsb_best_update(const qsb_state* st, void* stream) {
   const int grid = (int)((b.m + WPB - 1) / WPB);
   if (grid <= 0) return QSB_EINVAL;
   if (st->cost_dtype == QSB_I64)
-    best_kernel<int64_t, WPB><<<grid, 32 * WPB, 0, (cudaStream_t)stream>>>(b);
-  else if (st->cost_dtype == QSB_F64)
-    best_kernel<double, WPB><<<grid, 32 * WPB, 0, (cudaStream_t)stream>>>(b);
-  else
-    return QSB_EINVAL;
-  return launch_status();
+    return launch_pdl(best_kernel<int64_t, WPB>, grid, 32 * WPB, 0, (cudaStream_t)stream, b);
+  if (st->cost_dtype == QSB_F64)
+    return launch_pdl(best_kernel<double, WPB>, grid, 32 * WPB, 0, (cudaStream_t)stream, b);
+  return QSB_EINVAL;
 }
 
 int qsb_step(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co, void* stream) {

@@ -1096,6 +1096,9 @@ step_kernel(const __grid_constant__ StepArgs a) {
   // entry once, with no second (rescale) pass over the tile
   const bool defer = sizeof(VT) == 4 && G > 1 && a.vcol != nullptr;
 
+  // PDL: everything below may read what the previous kernel (coef_kernel,
+  // best_kernel, migrate_kernel, 2-opt) wrote
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
   const int nn = n * n;
