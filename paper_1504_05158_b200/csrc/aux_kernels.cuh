@@ -107,14 +107,27 @@ __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const volatile CT* sm = reinterpret_cast<const volatile CT*>(a.swarm_min);
-  const volatile int64_t* smi = a.swarm_min_idx;
+  // the other blocks' swarm minima, read from L2 (ld.cg), four per thread in
+  // flight before any compare; the best record's inputs fetched alongside
+  const CT* sm = reinterpret_cast<const CT*>(a.swarm_min);
+  const int64_t* smi = a.swarm_min_idx;
+  CT* gb = reinterpret_cast<CT*>(a.best_cost);
+  const int64_t t = *a.t_dev + 1;
+  const CT gb_old = *gb;
   CT bc = ct_max<CT>();
   int64_t bidx = INT64_MAX;
-  for (int64_t q = threadIdx.x; q < a.m; q += blockDim.x) {
-    const CT c = sm[q];
-    const int64_t i = smi[q];
-    if (lex_less(c, i, bc, bidx)) { bc = c; bidx = i; }
+  for (int64_t q0 = 0; q0 < a.m; q0 += 4 * (int64_t)blockDim.x) {
+    CT cv[4];
+    int64_t iv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = q0 + threadIdx.x + (int64_t)j * blockDim.x;
+      cv[j] = q < a.m ? __ldcg(sm + q) : ct_max<CT>();
+      iv[j] = q < a.m ? (int64_t)__ldcg((const long long*)smi + q) : INT64_MAX;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (lex_less(cv[j], iv[j], bc, bidx)) { bc = cv[j]; bidx = iv[j]; }
   }
   warp_lexmin(bc, bidx);
   __shared__ CT wc[WPB];
@@ -125,9 +138,7 @@ __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
     bc = lane < WPB ? wc[lane] : ct_max<CT>();
     bidx = lane < WPB ? wi[lane] : INT64_MAX;
     warp_lexmin(bc, bidx);
-    const int64_t t = *a.t_dev + 1;
-    CT* gb = reinterpret_cast<CT*>(a.best_cost);
-    const bool upd = bidx != INT64_MAX && bc < *gb;
+    const bool upd = bidx != INT64_MAX && bc < gb_old;
     if (upd)
       for (int c = lane; c < n; c += 32) a.best_perm[c] = a.perm_new[bidx * n + c];
     __syncwarp();

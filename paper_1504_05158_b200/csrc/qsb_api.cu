@@ -433,13 +433,24 @@ int qsb_best_update(const qsb_state* st, void* stream) {
   b.swarm_min = st->swarm_min;
   b.swarm_min_idx = st->swarm_min_idx;
   b.done = st->done;
-  constexpr int WPB = 8;
-  const int grid = (int)((b.m + WPB - 1) / WPB);
+  static int wpb = -1;
+  if (wpb < 0) {
+    const char* e = std::getenv("QSB_BEST_WPB");
+    wpb = (e && e[0] == '4') ? 4 : 8;
+  }
+  const int grid = (int)((b.m + wpb - 1) / wpb);
   if (grid <= 0) return QSB_EINVAL;
+  if (wpb == 4) {
+    if (st->cost_dtype == QSB_I64)
+      return launch_pdl(best_kernel<int64_t, 4>, grid, 32 * 4, 0, (cudaStream_t)stream, b);
+    if (st->cost_dtype == QSB_F64)
+      return launch_pdl(best_kernel<double, 4>, grid, 32 * 4, 0, (cudaStream_t)stream, b);
+    return QSB_EINVAL;
+  }
   if (st->cost_dtype == QSB_I64)
-    return launch_pdl(best_kernel<int64_t, WPB>, grid, 32 * WPB, 0, (cudaStream_t)stream, b);
+    return launch_pdl(best_kernel<int64_t, 8>, grid, 32 * 8, 0, (cudaStream_t)stream, b);
   if (st->cost_dtype == QSB_F64)
-    return launch_pdl(best_kernel<double, WPB>, grid, 32 * WPB, 0, (cudaStream_t)stream, b);
+    return launch_pdl(best_kernel<double, 8>, grid, 32 * 8, 0, (cudaStream_t)stream, b);
   return QSB_EINVAL;
 }
 
