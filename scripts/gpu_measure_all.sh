@@ -10,7 +10,7 @@ timeout 600 python bench.py --impl reference > gpurun_out/m/bench_reference.json
 timeout 300 python bench.py --preset config1 --no-cpu --steps 400 --graph > gpurun_out/m/bench_config1.json 2>> gpurun_out/m/err.log
 timeout 300 python bench.py --preset config2 --no-cpu --steps 200 > gpurun_out/m/bench_config2.json 2>> gpurun_out/m/err.log
 timeout 300 python bench.py --preset config4 --no-cpu --steps 200 > gpurun_out/m/bench_config4.json 2>> gpurun_out/m/err.log
-timeout 600 python bench.py --preset config5 --no-cpu --steps 30 --warmup 3 --e2e-steps 10 > gpurun_out/m/bench_config5.json 2>> gpurun_out/m/err.log
+timeout 600 python bench.py --preset config5 --no-cpu --steps 30 --warmup 3 > gpurun_out/m/bench_config5.json 2>> gpurun_out/m/err.log
 timeout 300 python bench.py --precision fp64 --no-cpu --steps 200 > gpurun_out/m/bench_config3_fp64.json 2>> gpurun_out/m/err.log
 timeout 300 python bench.py --velocity-only --no-cpu --steps 100 > gpurun_out/m/bench_velocity_n50.json 2>> gpurun_out/m/err.log
 timeout 300 python bench.py --preset config4 --velocity-only --no-cpu --steps 100 > gpurun_out/m/bench_velocity_n100_10k.json 2>> gpurun_out/m/err.log
