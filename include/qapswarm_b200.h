@@ -151,7 +151,8 @@ typedef struct qsb_migration {
   int32_t mode;              /* 0 single device, 1 plan+pack, 2 apply exchanged records */
   int32_t reserved;
   int64_t num_swarms_total;  /* m over all devices */
-  const int32_t* picks;      /* (rows, d): host_rng(seed, t).integers(0, S) per event */
+  const int32_t* picks;      /* (rows, d): host_rng(seed, t).integers(0, S) per event,
+                              * or NULL: the kernel draws them from `seed` (below) */
   int64_t picks_epoch0;      /* epoch (t / period) of picks row 0 */
   int64_t picks_rows;
   const void* all_pg_cost;   /* (m_total,) swarm-best costs in global order */
@@ -161,6 +162,7 @@ typedef struct qsb_migration {
   int64_t log_rows;
   int64_t* log_count;        /* (1,) events logged */
   int32_t* status;           /* (1,) set to 1 when picks has no row for t */
+  uint64_t seed;             /* SolverConfig.seed wrapped to uint64; used when picks == NULL */
 } qsb_migration;
 
 int qsb_version(void);
@@ -194,8 +196,17 @@ int qsb_best_update(const qsb_state* st, void* stream);
  * swaps perm/perm_new afterwards (engine.py:231-232). */
 int qsb_step(const qsb_state* st, const qsb_instance* inst, const qsb_coeffs* co, void* stream);
 
-/* Migration (migration.py:55-86) on the post-swap state. */
+/* Migration (migration.py:55-86) on the post-swap state.  With
+ * mig->picks == NULL the donor offsets are drawn on the device from the
+ * reference's host stream host_rng(seed, t) (streams.py:48-50), exactly as
+ * numpy's scalar Generator.integers(0, S) would draw them. */
 int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream);
+
+/* The d donor offsets of the migration event at iteration t (device int32
+ * out): host_rng(seed, t).integers(0, swarm_size) called d times
+ * (migration.py:82-84).  Parity / debug entry of the in-kernel draw. */
+int qsb_migration_picks(uint64_t seed, uint64_t t, int32_t d, int64_t swarm_size, int32_t* out,
+                        void* stream);
 
 /* 2-opt local search (north-star extension; no reference symbol, SURVEY.md
  * 8a a11) on st->perm_new / st->cost, integral instances only.  Per pass the

@@ -62,7 +62,8 @@ class QsbMigration(ctypes.Structure):
     _fields_ = [("d", _i32), ("period", _i32), ("mode", _i32), ("reserved", _i32),
                 ("num_swarms_total", _i64), ("picks", _vp), ("picks_epoch0", _i64),
                 ("picks_rows", _i64), ("all_pg_cost", _vp), ("plan", _vp), ("records", _vp),
-                ("log", _vp), ("log_rows", _i64), ("log_count", _vp), ("status", _vp)]
+                ("log", _vp), ("log_rows", _i64), ("log_count", _vp), ("status", _vp),
+                ("seed", _u64)]
 
 
 # name -> (restype, argtypes); every symbol of include/qapswarm_b200.h
@@ -84,6 +85,7 @@ SIGNATURES = {
                                   _i32, _vp]),
     "qsb_twoopt_many": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32]),
     "qsb_step_draws": (ctypes.c_int, [_u64, _u64, _i64, _i64, _i32, _vp, _vp]),
+    "qsb_migration_picks": (ctypes.c_int, [_u64, _u64, _i32, _i64, _vp, _vp]),
     "qsb_stats_work_bytes": (ctypes.c_size_t, []),
     "qsb_population_stats": (ctypes.c_int, [_vp, _i32, _i64, _dbl, _dbl, _i32, _vp, _i32, _vp,
                                             _vp, _vp, _vp]),

@@ -160,9 +160,11 @@ struct MigArgs {
   int d;                 // replacements per event
   int period;            // run only when t % period == 0 (0: unconditional)
   const int64_t* t_dev;  // current iteration (already advanced by best_kernel)
-  const int32_t* picks;  // (rows, d) donor offsets j = rng.integers(0, S)
+  const int32_t* picks;  // (rows, d) donor offsets j = rng.integers(0, S), or
+                         // NULL: drawn here from host_rng(seed, t) (host_picks)
   int64_t picks_e0;      // epoch of row 0 (epoch = t / period, or t if period == 0)
   int64_t picks_rows;
+  uint64_t seed;         // SolverConfig.seed wrapped to uint64 (device picks)
   const void* all_pg_cost;   // (m,) global swarm-best costs (== pg_cost on one device)
   const int16_t* perm;   // local current particles (post-swap)
   const void* cost;      // local current costs
@@ -175,9 +177,54 @@ struct MigArgs {
   int64_t* log_count;    // events written so far (device counter)
   int* status;           // set to 1 if the picks table has no row for t
   int mode;              // 0 fused (plan+apply), 1 plan+pack, 2 apply from rec
+  size_t picks_smem_off; // byte offset of the device picks in dynamic shared memory
 };
 
 constexpr int MIG_SORT_MAX = 8192;   // swarms sorted in shared memory (larger m: rank counting)
+
+// 32-bit draw j of a fresh numpy Generator(Philox(key = (seed, word1))):
+// numpy's Philox hands out the low then the high half of each 64-bit word,
+// words in counter order starting at counter 1 (numpy increments first).
+__device__ __forceinline__ uint32_t host_u32(uint64_t seed, uint64_t word1, uint64_t j) {
+  const PhiloxBlock b = philox4x64_10((j >> 3) + 1, seed, word1);
+  const uint64_t w = b.v[(j >> 1) & 3];
+  return (j & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
+}
+
+// The donor offsets of one migration event: d successive scalar calls
+// rng.integers(0, S) on host_rng(seed, t) (migration.py:82-84,
+// streams.py:48-50).  numpy bounds a 32-bit draw x by Lemire's method:
+// m = x * S, rejected while (m mod 2^32) < (2^32 - S) mod S, value m >> 32.
+// Draw k uses 32-bit word k unless an earlier draw was rejected, so every
+// thread takes its own word and, in the (probability <= d S / 2^32) case of
+// a rejection anywhere, one thread redraws the event sequentially.
+// Block-wide: every thread of the block must call it.
+__device__ void host_picks(uint64_t seed, uint64_t t, int d, int64_t S, int32_t* out) {
+  const uint64_t word1 = stream_word(3, t);
+  const uint32_t thr = (uint32_t)((0x100000000ULL - (uint64_t)S) % (uint64_t)S);
+  int rej = 0;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    const uint64_t m = (uint64_t)host_u32(seed, word1, (uint64_t)k) * (uint64_t)S;
+    rej |= (uint32_t)m < thr;
+    out[k] = (int32_t)(m >> 32);
+  }
+  if (__syncthreads_or(rej)) {
+    if (threadIdx.x == 0) {
+      uint64_t j = 0;
+      for (int k = 0; k < d; ++k) {
+        uint64_t m;
+        do { m = (uint64_t)host_u32(seed, word1, j++) * (uint64_t)S; } while ((uint32_t)m < thr);
+        out[k] = (int32_t)(m >> 32);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Debug / parity entry: the picks of iteration t into out (one block).
+__global__ void picks_kernel(uint64_t seed, uint64_t t, int d, int64_t S, int32_t* out) {
+  host_picks(seed, t, d, S, out);
+}
 
 // Stable ascending rank of every swarm cost (np.argsort(kind="stable")),
 // then rank k donates to rank m-1-k (migration.py:81-90).
@@ -188,7 +235,7 @@ __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
   if (a.period > 0 && (t % a.period) != 0) return;
   const int64_t epoch = a.period > 0 ? t / a.period : t;
   const int64_t row = epoch - a.picks_e0;
-  if (a.mode != 2 && (row < 0 || row >= a.picks_rows)) {
+  if (a.mode != 2 && a.picks && (row < 0 || row >= a.picks_rows)) {
     if (threadIdx.x == 0) *a.status = 1;
     return;
   }
@@ -222,6 +269,9 @@ __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
   }
   CT* sc = reinterpret_cast<CT*>(msm);
   int32_t* order = reinterpret_cast<int32_t*>(msm + align_up(m * sizeof(CT), 16));
+  // device picks after the sort scratch (qsb_migrate sizes the buffer)
+  int32_t* dpk = reinterpret_cast<int32_t*>(msm + a.picks_smem_off);
+  if (!a.picks) host_picks(a.seed, (uint64_t)t, a.d, a.S, dpk);
   const CT* allc = reinterpret_cast<const CT*>(a.all_pg_cost);
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) sc[i] = allc[i];
   __syncthreads();
@@ -265,7 +315,7 @@ __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
     }
   }
   __syncthreads();
-  const int32_t* picks = a.picks + row * a.d;
+  const int32_t* picks = a.picks ? a.picks + row * a.d : dpk;
   for (int k = threadIdx.x; k < a.d; k += blockDim.x) {
     const int64_t src = order[k];
     const int64_t dst = order[m - 1 - k];
@@ -416,7 +466,11 @@ __global__ void perm_to_mat_kernel(const PT* perm, int64_t P, int n, int8_t* x) 
 // Throughput-mode initialisation (NOT the reference's init stream): every
 // particle draws a Fisher-Yates permutation and U(-amp, amp) velocities from
 // Philox keyed (seed, 4<<56); particle rows are counter offsets, so the
-// result is independent of the device count.
+// result is independent of the device count.  Global particle p owns words
+// p (n^2 + n) + e: e < n^2 the velocity entries (row-major), then n - 1
+// shuffle draws, i = n-1 .. 1 swapping perm[i] with perm[min(floor(u (i+1)), i)]
+// (the reference's init_population, engine.py:150-156, draws a permuted
+// identity and U(-amp, amp) the same way, from its own sequential stream).
 template <typename VT>
 __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vstride, double amp,
                             int16_t* perm, VT* V) {
@@ -432,7 +486,9 @@ __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vst
       if (e < nn) {
         const uint64_t idx = base + (uint64_t)e;
         const double u = u64_to_unit(philox4x64_10((idx >> 2) + 1, seed, word1).v[idx & 3]);
-        const double v = -amp + 2.0 * amp * u;
+        // (-amp) + (2 amp) u with separate roundings (no FMA), so the oracle
+        // restates it in numpy (oracle.device_init)
+        const double v = __dadd_rn(-amp, __dmul_rn(__dmul_rn(2.0, amp), u));
         if constexpr (sizeof(VT) == 4) vp[e] = n <= WIDE_MAX_N ? (VT)wenc(v) : (VT)v;
         else vp[e] = (VT)v;
       } else {

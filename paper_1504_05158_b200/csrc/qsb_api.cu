@@ -491,14 +491,16 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
   a.log_count = mig->log_count;
   a.status = mig->status;
   a.mode = mig->mode;
+  a.seed = mig->seed;
   if (!a.plan || !a.status || (a.log && !a.log_count)) return QSB_EINVAL;
   if (a.mode == 0 && (a.m0 != 0 || a.m_local != a.m)) return QSB_EINVAL;
   if (a.mode == 2 && !a.rec) return QSB_EINVAL;
   const size_t csz = st->cost_dtype == QSB_F64 ? 8 : 8;
   size_t p2 = 1;
   while (p2 < (size_t)a.m) p2 <<= 1;
-  const size_t smem = align_up((size_t)a.m * csz, 16) +
-                      (p2 <= (size_t)MIG_SORT_MAX ? align_up(p2, 4) * 4 + p2 * 8 : (size_t)a.m * 4);
+  a.picks_smem_off = align_up(align_up((size_t)a.m * csz, 16) +
+                       (p2 <= (size_t)MIG_SORT_MAX ? align_up(p2, 4) * 4 + p2 * 8 : (size_t)a.m * 4), 16);
+  const size_t smem = a.picks_smem_off + (mig->picks ? 0 : align_up((size_t)a.d * 4, 16));
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
   if (st->cost_dtype == QSB_I64) {
@@ -510,6 +512,14 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
       cudaFuncSetAttribute(migrate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     migrate_kernel<double><<<1, 1024, smem, s>>>(a);
   }
+  return launch_status();
+}
+
+int qsb_migration_picks(uint64_t seed, uint64_t t, int32_t d, int64_t swarm_size, int32_t* out,
+                        void* stream) {
+  if (!out || d < 0 || swarm_size < 1 || swarm_size > 0xFFFFFFFFLL) return QSB_EINVAL;
+  if (d == 0) return QSB_OK;
+  picks_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(seed, t, d, swarm_size, out);
   return launch_status();
 }
 

@@ -34,6 +34,7 @@ import torch
 
 from . import _lib
 from .config import SX_CODES, PsoCoefficients, SolverConfig
+from .core import gap
 from .instance import device_format, is_integral
 from .migration import MigrationEvent, SwarmBestTable
 from .stats import PERCENTILE_RANKS, IterationStats, _ranks_sorted, collect
@@ -372,7 +373,8 @@ class _Runtime:
         # byte-sized entries with int32-safe sums: the 2-opt dp4a kernel
         mf, md = (int(fa.max()), int(da.max())) if fa.size else (0, 0)
         self.twoopt_bytes = bool(code == _lib.U16 and max(mf, md) < 256 and state.n * mf * md < 2**31)
-        self.key = (id(instance), config.coefficients, config.seed)
+        self.instance = instance
+        self.key = (config.coefficients, config.seed)
         c = config.coefficients
         self.coeffs = _lib.QsbCoeffs(c.c1, c.c2, c.c3, c.v_max, int(c.sv_mode == "norm"),
                                      SX_CODES[c.sx_mode], c.depth, 0, int(config.seed) & (2**64 - 1))
@@ -382,9 +384,15 @@ class _Runtime:
 
 
 def _runtime(state: PopulationState, instance, config: SolverConfig) -> _Runtime:
-    key = (id(instance), config.coefficients, config.seed)
+    key = (config.coefficients, config.seed)
     rt = state._inst
-    if rt is None or rt.key != key:
+    # keyed on the instance object itself (held by the runtime), not id():
+    # a collected instance's id can be reused by a different one
+    if rt is None or rt.instance is not instance or rt.key != key:
+        if rt is not None and rt.instance is not instance:
+            # the stored goals belong to the previous instance: the next
+            # step evaluates the full goal (no incremental update)
+            state.cost_current = False
         rt = _Runtime(state, instance, config)
         state._inst = rt
     return rt
@@ -453,50 +461,42 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
 
 # ------------------------------------------------------------- migration
 class _MigrationScratch:
-    """Device buffers of the migration phase plus a window of precomputed
-    donor picks (one row of d offsets per migration epoch)."""
+    """Device buffers of the migration phase.  The donor picks are drawn
+    inside migrate_kernel from the reference's host stream (seed, t), so no
+    host work is left in a migration epoch."""
 
-    CHUNK = 64
-
-    def __init__(self, state: PopulationState, d: int):
+    def __init__(self, state: PopulationState, d: int, log_rows: int = _LOG_EPOCHS):
         dev = state.device
         self.d = d
         self.device = dev
         self.plan = torch.zeros((d, 4), dtype=torch.int64, device=dev)
-        self.log = torch.zeros((_LOG_EPOCHS, d, 6), dtype=torch.float64, device=dev)
+        self.log = torch.zeros((log_rows, d, 6), dtype=torch.float64, device=dev)
         self.log_count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.records = torch.zeros((d, state.n + 1), dtype=torch.int64, device=dev)
-        self.picks = None
-        self.e0 = 0
-        self.rows = 0
         self.pending = 0          # epochs logged on the device, not yet drained
 
-    def ensure_picks(self, config: SolverConfig, t: int, swarm_size: int):
-        """Make sure the picks window holds epoch t // period."""
-        period = config.migration_period
-        e = t // period
-        if self.picks is not None and self.e0 <= e < self.e0 + self.rows:
-            return
-        last = (_ITER_LIMIT - 1) // period
-        rows = max(1, min(self.CHUNK, last - e + 1))
-        tab = np.stack([migration_picks(config.seed, (e + r) * period, self.d, swarm_size)
-                        for r in range(rows)])
-        self.picks = torch.from_numpy(tab).to(self.device)
-        self.e0, self.rows = e, rows
-
-
-def migration_picks(seed: int, iteration: int, d: int, swarm_size: int) -> np.ndarray:
-    """Donor offsets of one migration event: ``host_rng(seed, t).integers(0, S)``
-    drawn once per replacement, in rank order (migration.py:82-84)."""
-    rng = phase_rng(seed, PHASE_HOST, iteration)
-    return np.array([rng.integers(0, swarm_size) for _ in range(d)], dtype=np.int32)
+    def struct(self, state: PopulationState, config: SolverConfig) -> _lib.QsbMigration:
+        mig = _lib.QsbMigration()
+        mig.d, mig.period, mig.mode, mig.reserved = self.d, config.migration_period, 0, 0
+        mig.num_swarms_total = state.swarms
+        mig.picks, mig.picks_epoch0, mig.picks_rows = None, 0, 0    # drawn on the device
+        mig.seed = int(config.seed) & (2**64 - 1)
+        mig.all_pg_cost = state.d_pg_cost.data_ptr()
+        mig.plan, mig.records = self.plan.data_ptr(), self.records.data_ptr()
+        mig.log, mig.log_rows = self.log.data_ptr(), self.log.shape[0]
+        mig.log_count = self.log_count.data_ptr()
+        mig.status = self.status.data_ptr()
+        return mig
 
 
 def _drain_log(state: PopulationState):
     ms = state._mig
     if ms is None or ms.pending == 0:
         return
+    if int(ms.status.item()) != 0:
+        raise RuntimeError("migrate_kernel reported a missing donor-picks row (status "
+                           f"{int(ms.status.item())}); migration events were dropped")
     rows = ms.log[:ms.pending].cpu().numpy().reshape(-1, 6)
     for r in rows:
         state._migration_log.append(MigrationEvent(int(r[0]), int(r[1]), int(r[2]), int(r[3]),
@@ -506,24 +506,15 @@ def _drain_log(state: PopulationState):
 
 
 def migration_struct(state: PopulationState, config: SolverConfig, t: int) -> _lib.QsbMigration:
-    """C descriptor of the migration event at iteration t (picks prepared)."""
+    """C descriptor of the migration event at iteration t."""
     d = config.migration_depth
     if state._mig is None or state._mig.d != d:
         _drain_log(state)
         state._mig = _MigrationScratch(state, d)
     ms = state._mig
-    if ms.pending >= _LOG_EPOCHS:
+    if ms.pending >= ms.log.shape[0]:
         _drain_log(state)
-    ms.ensure_picks(config, t, state.swarm_size)
-    mig = _lib.QsbMigration()
-    mig.d, mig.period, mig.mode, mig.reserved = d, config.migration_period, 0, 0
-    mig.num_swarms_total = state.swarms
-    mig.picks, mig.picks_epoch0, mig.picks_rows = ms.picks.data_ptr(), ms.e0, ms.rows
-    mig.all_pg_cost = state.d_pg_cost.data_ptr()
-    mig.plan, mig.records = ms.plan.data_ptr(), ms.records.data_ptr()
-    mig.log, mig.log_rows, mig.log_count = ms.log.data_ptr(), _LOG_EPOCHS, ms.log_count.data_ptr()
-    mig.status = ms.status.data_ptr()
-    return mig
+    return ms.struct(state, config)
 
 
 def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchange=None):
@@ -586,6 +577,22 @@ def collect_device(state: PopulationState, time_ms: float, bins: int = 60,
 
 
 # ------------------------------------------------------------------ step
+def _hints(state: PopulationState, rt: "_Runtime", coeffs: PsoCoefficients) -> int:
+    """Launch hints the state guarantees for its next step (QSB_HINT_*)."""
+    # |c1 v| <= v_max for every stored v => the bulk-row clamp is a no-op
+    hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
+    if state.cost_current and state.integral:
+        hints |= _lib.HINT_COST_CURRENT
+        if rt.symmetric_int:
+            hints |= _lib.HINT_SYMMETRIC
+    return hints
+
+
+def _post_step_v_bound(coeffs: PsoCoefficients) -> float:
+    """After S_v every entry is clamped to v_max, or normalised to |v| <= 1."""
+    return (1.0 + 1e-6) if coeffs.sv_mode == "norm" else coeffs.v_max
+
+
 def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
          timer=None) -> PopulationState:
     """Advance one iteration (engine.py:181-244): the fused velocity /
@@ -605,13 +612,7 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     rt = _runtime(state, instance, config)
     stream = state.stream()
     cs = state.c_state()
-    # |c1 v| <= v_max for every stored v => the bulk-row clamp is a no-op
-    hints = _lib.HINT_V_BOUNDED if coeffs.c1 * state.v_bound * (1 + 1e-6) <= coeffs.v_max else 0
-    if state.cost_current and state.integral:
-        hints |= _lib.HINT_COST_CURRENT
-        if rt.symmetric_int:
-            hints |= _lib.HINT_SYMMETRIC
-    rt.coeffs.hints = hints
+    rt.coeffs.hints = _hints(state, rt, coeffs)
     passes = config.two_opt_passes
     if passes and not state.integral:
         raise ValueError("two_opt_passes requires an integral instance")
@@ -633,8 +634,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
         state.launches += 1
     _lib.call("qsb_best_update", cs, stream)
     state.launches += 3      # draw pre-pass + fused step + best update
-    # after S_v every entry is clamped to v_max, or normalised to |v| <= 1
-    state.v_bound = (1.0 + 1e-6) if coeffs.sv_mode == "norm" else coeffs.v_max
+    state.v_bound = _post_step_v_bound(coeffs)
+    state.cost_current = True     # cost[p] is now the goal of the new position
     state.swap_positions()
     state._host_best = None
     if config.migration_factor > 0.0 and t % config.migration_period == 0:
@@ -653,99 +654,106 @@ def _due_epochs(config: SolverConfig, t0: int, t1: int) -> int:
     return t1 // P - t0 // P
 
 
-def step_many(state: PopulationState, instance, config: SolverConfig, steps: int) -> PopulationState:
-    """Advance ``steps`` iterations, replaying one CUDA graph that holds two
-    iterations (so perm / perm_new return to their buffers) with migration
-    decided on the device (t % migration_period).  Results are identical to
-    calling :func:`step` ``steps`` times; the host only launches the graph.
-    Single-device states only."""
+def _graph_span(config: SolverConfig) -> int:
+    """Iterations held by one captured graph: even (perm / perm_new return
+    to their buffers) and a multiple of the migration period, so a graph
+    that starts at t % span == 0 has its migration launches at fixed slots."""
+    if config.migration_factor <= 0.0 or config.migration_depth <= 0:
+        return 2
+    return math.lcm(2, config.migration_period)
+
+
+def step_many(state: PopulationState, instance, config: SolverConfig, steps: int,
+              exchange=None) -> PopulationState:
+    """Advance ``steps`` iterations by replaying a CUDA graph of
+    :func:`_graph_span` iterations, with the migration launches (and, for
+    sharded states, the ``exchange`` collectives) captured at their slots.
+    Results are identical to calling :func:`step` ``steps`` times; the host
+    only launches the graph.  Steps before the first aligned iteration and
+    after the last whole graph run eagerly."""
     if steps <= 0:
         return state
-    if state.local_particles != state.num_particles:
-        raise ValueError("step_many drives single-device states; use step() with an exchange")
-    # one eager iteration fixes the launch hints (bounded velocity, current costs)
-    step(state, instance, config)
-    steps -= 1
-    pairs = steps // 2
-    if pairs >= 2:
+    sharded = state.local_particles != state.num_particles
+    if sharded and exchange is None and _due_epochs(config, state.t, state.t + steps):
+        raise ValueError("a sharded state with migration needs the cross-device exchange")
+    span = _graph_span(config)
+    # eager steps up to an aligned start (the first one also settles the
+    # launch hints: velocity bound and current costs)
+    while steps > 0 and (state.t == 0 or state.t % span != 0 or not state.cost_current):
+        step(state, instance, config, exchange=exchange)
+        steps -= 1
+    reps = steps // span
+    if reps >= 1:
         rt = _runtime(state, instance, config)
-        t0 = state.t
+        coeffs = config.coefficients
+        hints = _hints(state, rt, coeffs)     # valid for every later step (post-S_v bound)
+        rt.coeffs.hints = hints
         d = config.migration_depth if config.migration_factor > 0.0 else 0
-        mig = None
-        # a captured graph without migration is reusable while the buffers line up
-        key = (rt.key, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr())
+        # rt: the runtime object itself (its device instance is captured)
+        key = (rt, hints, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr(),
+               exchange is None)
         cached = getattr(state, "_graph_cache", None)
-        if d == 0 and cached is not None and cached[0] == key:
-            graph = cached[1]
-            for _ in range(pairs):
-                graph.replay()
-            passes = config.two_opt_passes
-            state.launches += pairs * 2 * (3 + (1 if passes else 0))
-            state.t = t0 + 2 * pairs
-            state._host_best = None
-            for _ in range(steps - 2 * pairs):
-                step(state, instance, config)
-            return state
+        mig = None
         if d > 0:
-            _drain_log(state)
-            ms = _MigrationScratch(state, d)
-            epochs = _due_epochs(config, t0, t0 + 2 * pairs)
-            ms.log = torch.zeros((max(epochs, 1), d, 6), dtype=torch.float64, device=state.device)
-            e0 = (t0 + 1 + config.migration_period - 1) // config.migration_period
-            rows = max(1, (t0 + 2 * pairs) // config.migration_period - e0 + 1)
-            tab = np.stack([migration_picks(config.seed, (e0 + r) * config.migration_period, d,
-                                            state.swarm_size) for r in range(rows)])
-            ms.picks = torch.from_numpy(tab).to(state.device)
-            ms.e0, ms.rows = e0, rows
-            state._mig = ms
-            mig = _lib.QsbMigration()
-            mig.d, mig.period, mig.mode, mig.reserved = d, config.migration_period, 0, 0
-            mig.num_swarms_total = state.swarms
-            mig.picks, mig.picks_epoch0, mig.picks_rows = ms.picks.data_ptr(), ms.e0, ms.rows
-            mig.all_pg_cost = state.d_pg_cost.data_ptr()
-            mig.plan, mig.records = ms.plan.data_ptr(), ms.records.data_ptr()
-            mig.log, mig.log_rows = ms.log.data_ptr(), ms.log.shape[0]
-            mig.log_count = ms.log_count.data_ptr()
-            mig.status = ms.status.data_ptr()
-        passes = config.two_opt_passes
-        flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
-        tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
-              | (_lib.TWOOPT_BYTES if rt.twoopt_bytes else 0))
-        cs_a = state.c_state()
-        cs_b = _lib.QsbState.from_buffer_copy(cs_a)
-        cs_b.perm, cs_b.perm_new = cs_a.perm_new, cs_a.perm
-        graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(state.device)
-        side.wait_stream(torch.cuda.current_stream(state.device))
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(graph, stream=side):
-                s = side.cuda_stream
-                for cs in (cs_a, cs_b):
-                    _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, flags, None, 0, 2, None, 0, s)
-                    if passes:
-                        _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, s)
-                    _lib.call("qsb_best_update", cs, s)
-                    if mig is not None:
-                        mst = _lib.QsbState.from_buffer_copy(cs)
-                        mst.perm = cs.perm_new           # migration reads the post-swap positions
-                        _lib.call("qsb_migrate", mst, mig, s)
-        torch.cuda.current_stream(state.device).wait_stream(side)
-        for _ in range(pairs):
+            if state._mig is None or state._mig.d != d:
+                _drain_log(state)
+                state._mig = _MigrationScratch(state, d)
+            # room in the device log for every epoch of this call
+            need = state._mig.pending + _due_epochs(config, state.t, state.t + reps * span)
+            if need > state._mig.log.shape[0]:
+                _drain_log(state)
+                need = _due_epochs(config, state.t, state.t + reps * span)
+                if need > state._mig.log.shape[0]:
+                    state._mig = _MigrationScratch(state, d, log_rows=need)
+                    cached = None
+        if cached is not None and cached[0] == key and cached[2] is state._mig:
+            graph = cached[1]
+        else:
+            passes = config.two_opt_passes
+            flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
+            tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
+                  | (_lib.TWOOPT_BYTES if rt.twoopt_bytes else 0))
+            cs_a = state.c_state()
+            cs_b = _lib.QsbState.from_buffer_copy(cs_a)
+            cs_b.perm, cs_b.perm_new = cs_a.perm_new, cs_a.perm
+            if d > 0:
+                mig = state._mig.struct(state, config)
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(state.device)
+            side.wait_stream(torch.cuda.current_stream(state.device))
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    s = side.cuda_stream
+                    for i in range(span):
+                        cs = cs_a if i % 2 == 0 else cs_b
+                        _lib.call("qsb_step_phases", cs, rt.inst, rt.coeffs, flags, None, 0, 2,
+                                  None, 0, s)
+                        if passes:
+                            _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, s)
+                        _lib.call("qsb_best_update", cs, s)
+                        if mig is not None and (i + 1) % config.migration_period == 0:
+                            mst = _lib.QsbState.from_buffer_copy(cs)
+                            mst.perm = cs.perm_new           # migration reads the post-swap positions
+                            if exchange is None:
+                                _lib.call("qsb_migrate", mst, mig, s)
+                            else:
+                                exchange(state, mig, cstate=mst)
+            torch.cuda.current_stream(state.device).wait_stream(side)
+            state._graph_cache = (key, graph, state._mig, mig)
+        for _ in range(reps):
             graph.replay()
-        torch.cuda.current_stream(state.device).wait_stream(side)
-        state.launches += pairs * 2 * (3 + (1 if passes else 0))
-        state.t = t0 + 2 * pairs
-        if mig is not None:
-            state._mig.pending = _due_epochs(config, t0, t0 + 2 * pairs)
-            _drain_log(state)
-            state._mig = None          # later eager steps get a standard scratch
+        passes = config.two_opt_passes
+        epochs = _due_epochs(config, state.t, state.t + reps * span)
+        state.launches += reps * span * (3 + (1 if passes else 0)) \
+            + epochs * (1 if exchange is None else 2)
+        state.t += reps * span
+        if state._mig is not None:
+            state._mig.pending += epochs
+        state.v_bound = _post_step_v_bound(coeffs)
         state._host_best = None
-        steps -= 2 * pairs
-        state._graph_keepalive = graph
-        if mig is None:
-            state._graph_cache = (key, graph)
+        steps -= reps * span
     for _ in range(steps):
-        step(state, instance, config)
+        step(state, instance, config, exchange=exchange)
     return state
 
 
@@ -768,13 +776,6 @@ class RunResult:
         if self.iterations_run == 0:
             return 0.0
         return 1000.0 * self.total_seconds / self.iterations_run
-
-
-def gap(cost: float, reference: float) -> float:
-    """(cost - reference) / reference (core.py:90-94)."""
-    if reference <= 0:
-        raise ValueError(f"reference must be positive, got {reference}")
-    return (cost - reference) / reference
 
 
 def run(config: SolverConfig, instance, collect_stats: bool = True, device=None) -> RunResult:

@@ -67,15 +67,20 @@ def make_exchange(world: int, group=None):
     """Cross-device migration hook for ``engine.step(..., exchange=...)``."""
     from . import _lib
 
-    def exchange(state, mig):
+    def exchange(state, mig, cstate=None):
+        """``cstate``: the C state to migrate on (post-swap positions); the
+        state's current one by default.  CUDA-graph capture (engine.step_many)
+        passes the captured slot's state; the collectives are then captured
+        too, which needs NCCL (gloo runs eagerly only)."""
+        cs = cstate if cstate is not None else state.c_state()
         full = gather_swarm_costs(state.d_pg_cost, state.swarms, world, group)
         mig.all_pg_cost = full.data_ptr()
-        stream = state.stream()
+        stream = torch.cuda.current_stream(state.device).cuda_stream
         mig.mode = 1
-        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+        _lib.call("qsb_migrate", cs, mig, stream)
         exchange_records(state._mig.records, group)
         mig.mode = 2
-        _lib.call("qsb_migrate", state.c_state(), mig, stream)
+        _lib.call("qsb_migrate", cs, mig, stream)
         state._keep_alive = full
 
     return exchange

@@ -165,10 +165,21 @@ def test_collect_all_swarms_shape(golden_instances):
 
 
 # ------------------------------------------------------------- migration
-def test_migration_picks_match_reference_host_stream():
+def test_device_picks_algorithm_matches_reference_host_stream():
+    """migrate_kernel's in-kernel donor draw (Lemire over the Philox halves,
+    restated in oracle.lemire_picks) equals the reference's scalar
+    rng.integers(0, S) calls: golden vectors plus random keys, including a
+    swarm size whose rejection threshold is non-zero and a wrapped seed."""
     g = np.load(GOLDEN / "draws.npz")
     for i, (seed, t, S, d) in enumerate([(1, 10, 100, 264), (3, 5, 20, 16), (5, 1, 10, 1)]):
-        assert np.array_equal(engine.migration_picks(seed, t, d, S), g[f"host{i}"])
+        assert np.array_equal(orc.lemire_picks(seed, t, d, S), g[f"host{i}"])
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        seed = int(rng.integers(-2**40, 2**40))
+        t = int(rng.integers(0, 2**32))
+        S = int(rng.choice([1, 2, 3, 7, 100, 1000, 65535, 65536, 3 * 2**20 + 1]))
+        d = int(rng.integers(1, 300))
+        assert np.array_equal(orc.lemire_picks(seed, t, d, S), orc.migration_picks(seed, t, d, S))
 
 
 def test_migrate_validation_messages():

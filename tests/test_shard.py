@@ -84,7 +84,7 @@ def _worker(rank, world, port, swarms, S, seed, out):
         pg_costs_l = st.pg_costs[m0:m1].copy()
         full = shard.gather_swarm_costs(torch.from_numpy(pg_costs_l), swarms, world).numpy()
         assert np.array_equal(full, st.pg_costs)
-        picks = engine.migration_picks(seed, t, d, S)
+        picks = orc.migration_picks(seed, t, d, S)
         plan, rec = plan_pack(full, picks, S, m0, ml, perms_l, costs_l, n)
         rec_t = shard.exchange_records(torch.from_numpy(rec))
         apply(plan, rec_t.numpy(), m0, ml, pg_perms_l, pg_costs_l)
