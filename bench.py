@@ -49,6 +49,10 @@ def parse():
                     help="steps of the end-to-end (public API) measurement; default = --steps, "
                          "run on a fresh population over the same iterations as the device-timed "
                          "window (0 = skip)")
+    ap.add_argument("--host-steps", type=int, default=20,
+                    help="steps of the host-buffer end-to-end leg (qsb_step_host); 0 = skip")
+    ap.add_argument("--fp64-steps", type=int, default=20,
+                    help="steps of the fp64 parity-mode throughput window (value_fp64); 0 = skip")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--velocity-only", action="store_true",
@@ -262,19 +266,22 @@ def cpu_sample(args, seconds, swarms=8, steps_cap=1000, warm=1):
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU restatement of the reference's step
+    (oracle/, C + OpenMP over particles like the numba prange, fp64, the
+    O(n^3) aggregation of _batch.py) on the SAME workload -- every particle
+    of the config -- with all host threads.  Steps and warm-up are the
+    caller's, capped (40 / 5) so a default run stays within minutes."""
     if rank != 0:
         return
-    import numpy as np
     from oracle import oracle as orc
     import paper_1504_05158_b200 as qsb
     inst = qsb.taillard_uniform(args.n)
-    swarms = max(8, args.swarms // 10)
-    cfg = config(args, swarms=swarms, precision="fp64")
+    cfg = config(args, precision="fp64")
     st = orc.init_population(cfg.swarms, cfg.swarm_size, args.n, inst.flow, inst.distance,
                              seed=cfg.seed, amp=cfg.init_velocity_amplitude)
     kw = orc.coeff_kwargs(cfg)
-    steps = min(args.steps, 30)
-    warm = min(args.warmup, 3)
+    steps = min(args.steps, 40)
+    warm = min(args.warmup, 5)
     for _ in range(warm):
         orc.step(st, inst.flow, inst.distance, **kw)
     t0 = time.perf_counter()
@@ -283,14 +290,19 @@ def run_reference(args, rank, world):
     dt = time.perf_counter() - t0
     P = cfg.num_particles
     value = P * steps / dt
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000 * dt / steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload(args, world),
+    wl = workload(args, world)
+    wl["precision"] = "fp64"
+    wl["init"] = "reference (numpy init stream)"
+    line = {"impl": "reference", "metric": METRIC if args.preset == "config3" else
+            f"particle-iterations/sec (QAP n={args.n}, {P} particles, {args.preset})",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": 1000 * dt / steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": wl,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc.num_threads(),
                              "kind": "port",
-                             "sample": f"{swarms} swarms x {cfg.swarm_size} particles per step "
-                                       f"(1/10 of the workload), fp64 reference arithmetic"},
+                             "sample": f"the full workload: {cfg.swarms} swarms x {cfg.swarm_size} "
+                                       f"particles, iterations {warm + 1}-{warm + steps}, fp64 "
+                                       "reference arithmetic, all host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -420,7 +432,7 @@ def main():
     # ---- end to end through the public API: step() + D2H of the step's
     # per-particle costs and best record, synchronised every step
     e2e_steps = (args.steps if args.e2e_steps < 0 else args.e2e_steps) if flags is None else 0
-    e2e = None
+    e2e_resident = None
     if e2e_steps:
         # a fresh population, warmed up like the device-timed run, so the
         # end-to-end window covers the same iterations (W+1 .. W+K)
@@ -471,7 +483,7 @@ def main():
         wt = torch.tensor([w], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
-        e2e = {"value": P_total * e2e_steps / float(wt[0]), "unit": UNIT,
+        e2e_resident = {"value": P_total * e2e_steps / float(wt[0]), "unit": UNIT,
                "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(host_cost[0].numel() * host_cost[0].element_size()
                                          + host_best[0].element_size()),
@@ -534,6 +546,69 @@ def main():
 
     best = shard.merge_best(state.best_cost, state.best_iteration, 0, state.best_perm, world,
                             dev) if world > 1 else None
+    best_cost = best.cost if best else state.best_cost
+    # ---- end to end through the reference-facing C-ABI on HOST buffers:
+    # host.step_host (qsb_step_host) on the reference's PopulationState
+    # layout in pinned host memory -- f64 V, int8 0/1 matrices, int64 perms
+    # -- shipped to the device and back every step (fp64 reference
+    # arithmetic: the host layout is the reference's float64 state)
+    e2e = None
+    value_fp64 = None
+    host_steps = min(args.host_steps, args.steps) if (flags is None and world == 1) else 0
+    fp64_steps = args.fp64_steps if (flags is None and world == 1) else 0
+    if (host_steps and args.two_opt == 0) or fp64_steps:
+        del state
+        torch.cuda.empty_cache()
+        cfg64 = config(args, precision="fp64")
+        st64 = qsb.init_population(cfg64, inst, device=dev, swarm_range=(lo, hi))
+        for _ in range(args.warmup):
+            qsb.step(st64, inst, cfg64, exchange=exchange)
+        if fp64_steps:
+            # ---- the fp64 parity mode (bit-identical to the reference),
+            # device-resident, same workload, iterations W+1 .. W+K64
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(fp64_steps):
+                qsb.step(st64, inst, cfg64, exchange=exchange)
+            e1.record()
+            torch.cuda.synchronize()
+            ms64 = e0.elapsed_time(e1)
+            value_fp64 = {"value": P_total * fp64_steps / (ms64 / 1000.0), "unit": UNIT,
+                          "ms_per_step": ms64 / fp64_steps, "steps": fp64_steps,
+                          "iterations": f"{args.warmup + 1}-{args.warmup + fp64_steps}",
+                          "how": "precision='fp64' (bit-identical to the reference), device-"
+                                 "resident, CUDA events around the steps"}
+    if host_steps and args.two_opt == 0:
+        from paper_1504_05158_b200 import host
+        hp = host.HostPopulation.from_state(st64, cfg64)
+        del st64
+        torch.cuda.empty_cache()
+        host.step_host(hp, inst, cfg64)            # first call allocates the device buffers
+        torch.cuda.synchronize()
+        bytes_in = bytes_out = 0
+        w0 = time.perf_counter()
+        for _ in range(host_steps):
+            mig = cfg64.migration_factor > 0 and (hp.t + 1) % cfg64.migration_period == 0
+            bi, bo = hp.transfer_bytes(inst, migrate=mig)
+            bytes_in += bi
+            bytes_out += bo
+            host.step_host(hp, inst, cfg64)
+        w = time.perf_counter() - w0
+        e2e = {"value": P_total * host_steps / w, "unit": UNIT,
+               "h2d_bytes_per_step": int(bytes_in / host_steps),
+               "d2h_bytes_per_step": int(bytes_out / host_steps),
+               "steps": host_steps, "iterations": f"{hp.t - host_steps + 1}-{hp.t}",
+               "pcie_gb_s": (bytes_in + bytes_out) / w / 1e9,
+               "how": "host.step_host -> qsb_step_host (include/qapswarm_b200.h): one reference "
+                      "engine.step on the reference's host PopulationState (pinned numpy buffers: "
+                      "f64 V, int8 X/X_new/PL and swarm-best matrices, int64 perms/costs); every "
+                      "step copies the state host->device and the results device->host (8 "
+                      "swarm-aligned chunks, copies overlapped with the fused fp64 step, "
+                      "migration on the device); wall clock, synchronous calls; fp64 reference "
+                      "arithmetic (the host layout is the reference's float64 state)"}
+
     if rank == 0:
         metric = METRIC if args.preset == "config3" else \
             f"particle-iterations/sec (QAP n={args.n}, {P_total} particles, {args.preset})"
@@ -549,9 +624,10 @@ def main():
                        if use_graph and vbytes < 2 * L2_BYTES else
                        "> 2 x L2 (126 MB): inputs larger than L2"))),
                 "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clock_rec,
+                "e2e": e2e, "e2e_resident": e2e_resident, "value_fp64": value_fp64,
+                "gpu_launches": launches, "clocks": clock_rec,
                 "roofline_twoopt": roofline2,
-                "best_cost": best.cost if best else state.best_cost}
+                "best_cost": best_cost}
         if flags is not None:
             line["metric"] = "velocity/normalise phase HBM throughput"
         print(json.dumps(line), flush=True)

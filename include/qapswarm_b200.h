@@ -273,6 +273,54 @@ int qsb_twoopt_many(int64_t* perms, const int64_t* flow, const int64_t* distance
 /* streams.step_draws(seed, iteration, num_particles, n) (streams.py:53-64). */
 int qsb_step_draws_host(uint64_t seed, uint64_t t, int64_t P, int32_t n, double* out);
 
+/* The reference's PopulationState (engine.py:85-124) in HOST memory, in the
+ * reference's own layout: float64 velocities, int8 0/1 matrices
+ * X[k, i] = (perm[i] == k), int64 permutations, int64 (integral instance)
+ * or float64 costs.  Pinned (page-locked) buffers transfer fastest; any
+ * host memory works. */
+typedef struct qsb_host_population {
+  int32_t n;
+  int32_t cost_dtype;        /* QSB_I64 or QSB_F64 */
+  int64_t num_particles, swarm_size, num_swarms;
+  double* V;                 /* (P, n, n) in/out */
+  int8_t* X_new;             /* (P, n, n) out: next positions (X is not read:
+                              * perms is its exact vector view, core.py:5-6) */
+  int8_t* PL;                /* (P, n, n) in/out: rows of improved particles */
+  int64_t* perms;            /* (P, n) in: current positions */
+  int64_t* perms_new;        /* (P, n) out */
+  int64_t* pl_perms;         /* (P, n) in/out */
+  void* cost;                /* (P,) out: goal of perms_new */
+  void* pl_cost;             /* (P,) in/out */
+  uint8_t* improved;         /* (P,) out: cost < pl_cost this step */
+  int8_t* pg_mats;           /* (m, n, n) in/out: swarm bests */
+  int64_t* pg_perms;         /* (m, n) in/out */
+  void* pg_costs;            /* (m,) in/out */
+  int64_t* best_perm;        /* (n,) in/out: global best record */
+  void* best_cost;           /* (1,) in/out */
+  int64_t* best_iteration;   /* (1,) in/out */
+} qsb_host_population;
+
+/* A QAP instance in host memory (qaplib.QapInstance): int64 or float64. */
+typedef struct qsb_host_instance {
+  int32_t n;
+  int32_t mat_dtype;         /* QSB_I64 or QSB_F64 */
+  const void* flow;
+  const void* distance;
+} qsb_host_instance;
+
+/* One engine.step (engine.py:181-244) on host buffers: the step draws for
+ * iteration t (streams.py:53-64), velocity (_batch.py:30-58), aggregation
+ * (_batch.py:61-183), goal (_batch.py:186-197), personal / swarm / global
+ * bests (engine.py:210-229) and, when migrate_d > 0, migration
+ * (migration.py:55-86, donor picks from host_rng(seed, t)); the caller then
+ * swaps X <-> X_new and perms <-> perms_new (engine.py:231-232).  fp64
+ * parity arithmetic: results are bit-identical to the reference's step.
+ * migration_log (migrate_d x 6 doubles) receives the MigrationEvent fields.
+ * Synchronous; the particles stream through the device in swarm-aligned
+ * chunks (QSB_HOST_CHUNKS, default 8) with copies and compute overlapped. */
+int qsb_step_host(qsb_host_population* hp, const qsb_host_instance* inst, const qsb_coeffs* co,
+                  uint64_t t, int32_t migrate_d, double* migration_log);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,18 @@ class QsbMigration(ctypes.Structure):
                 ("seed", _u64)]
 
 
+class QsbHostPopulation(ctypes.Structure):
+    _fields_ = [("n", _i32), ("cost_dtype", _i32), ("num_particles", _i64), ("swarm_size", _i64),
+                ("num_swarms", _i64), ("V", _vp), ("X_new", _vp), ("PL", _vp), ("perms", _vp),
+                ("perms_new", _vp), ("pl_perms", _vp), ("cost", _vp), ("pl_cost", _vp),
+                ("improved", _vp), ("pg_mats", _vp), ("pg_perms", _vp), ("pg_costs", _vp),
+                ("best_perm", _vp), ("best_cost", _vp), ("best_iteration", _vp)]
+
+
+class QsbHostInstance(ctypes.Structure):
+    _fields_ = [("n", _i32), ("mat_dtype", _i32), ("flow", _vp), ("distance", _vp)]
+
+
 # name -> (restype, argtypes); every symbol of include/qapswarm_b200.h
 SIGNATURES = {
     "qsb_version": (ctypes.c_int, []),
@@ -98,6 +110,9 @@ SIGNATURES = {
     "qsb_cost_many_i64": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32]),
     "qsb_cost_many_f64": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i32]),
     "qsb_step_draws_host": (ctypes.c_int, [_u64, _u64, _i64, _i32, _vp]),
+    "qsb_step_host": (ctypes.c_int, [ctypes.POINTER(QsbHostPopulation),
+                                     ctypes.POINTER(QsbHostInstance), ctypes.POINTER(QsbCoeffs),
+                                     _u64, _i32, _vp]),
 }
 
 _lib = None

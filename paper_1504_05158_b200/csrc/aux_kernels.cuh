@@ -498,8 +498,8 @@ __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vst
     if (lane == 0) {
       int16_t* pp = perm + p * n;
       for (int i = 0; i < n; ++i) pp[i] = (int16_t)i;
-      DrawRow dr; dr.inj = nullptr; dr.seed = seed; dr.word1 = word1;
-      dr.base = base + (uint64_t)nn; dr.cached = ~0ULL;
+      DrawCache dr;
+      dr.init(DrawKey{nullptr, seed, word1, base + (uint64_t)nn});
       for (int i = n - 1; i > 0; --i) {
         long long j = (long long)(dr.at(n - 1 - i) * (double)(i + 1));
         if (j > i) j = i;

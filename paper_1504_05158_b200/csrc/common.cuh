@@ -65,26 +65,48 @@ __host__ __device__ __forceinline__ uint64_t stream_word(uint64_t phase, uint64_
   return (phase << 56) | (t << 24);
 }
 
-// Lazily evaluated per-particle draw row of streams.step_draws: column k of
-// particle row `row` is word row*(2+2n)+k.  Caches one Philox block so
-// consecutive draws cost one block per four.  Injected rows (tests replaying
-// fixed draws, or the reference-layout aggregate entry point) bypass Philox.
-struct DrawRow {
+// Per-particle draw row of streams.step_draws: column k of particle row
+// `row` is word row*(2+2n)+k.  DrawKey is plain values (it stays in
+// registers; an address-taken object would live in local memory, which the
+// per-particle hot path then writes every particle).  draw_at evaluates one
+// Philox block per call -- tie draws are rare; sequential runs of draws
+// (pick-column shuffles, the device init) use DrawCache, which keeps the
+// last block.  Injected rows (tests replaying fixed draws, the
+// reference-layout aggregate entry point) bypass Philox.
+struct DrawKey {
   const double* inj;   // nullable
   uint64_t seed, word1;
   uint64_t base;       // first word index of this particle's row
+};
+
+__device__ __forceinline__ double word_unit(const PhiloxBlock& b, unsigned l) {
+  const uint64_t w = l == 0 ? b.v[0] : l == 1 ? b.v[1] : l == 2 ? b.v[2] : b.v[3];
+  return u64_to_unit(w);
+}
+
+// out of line: several call sites (tie draws) in the step kernel
+__device__ __noinline__ double draw_at(const double* inj, uint64_t seed, uint64_t word1, uint64_t base,
+                                       int k) {
+  if (inj) return inj[k];
+  const uint64_t idx = base + (uint64_t)k;
+  return word_unit(philox_block_call((idx >> 2) + 1, seed, word1), (unsigned)(idx & 3));
+}
+
+__device__ __forceinline__ double draw_at(const DrawKey& d, int k) {
+  return draw_at(d.inj, d.seed, d.word1, d.base, k);
+}
+
+struct DrawCache {
+  DrawKey key;
   uint64_t cached;     // block index held in blk (UINT64_MAX = none)
   PhiloxBlock blk;
-
-  // out of line: several call sites (tie draws) in the step kernel
-  __device__ __noinline__ double at(int k) {
-    if (inj) return inj[k];
-    const uint64_t idx = base + (uint64_t)k;
+  __device__ __forceinline__ void init(const DrawKey& k) { key = k; cached = ~0ULL; }
+  __device__ __forceinline__ double at(int k) {
+    if (key.inj) return key.inj[k];
+    const uint64_t idx = key.base + (uint64_t)k;
     const uint64_t b = idx >> 2;
-    if (b != cached) { blk = philox_block_call(b + 1, seed, word1); cached = b; }
-    const unsigned l = (unsigned)(idx & 3);
-    const uint64_t w = l == 0 ? blk.v[0] : l == 1 ? blk.v[1] : l == 2 ? blk.v[2] : blk.v[3];
-    return u64_to_unit(w);
+    if (b != cached) { blk = philox_block_call(b + 1, key.seed, key.word1); cached = b; }
+    return word_unit(blk, (unsigned)(idx & 3));
   }
 };
 

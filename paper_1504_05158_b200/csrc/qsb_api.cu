@@ -24,6 +24,9 @@ static int cuda_status(cudaError_t e) {
 
 static int launch_status() { return cuda_status(cudaGetLastError()); }
 
+// CUDA errors of the other translation unit (host_step.cu)
+void qsb_note_cuda_error(int e) { g_last_cuda = e; }
+
 static int num_sms() {
   static int sms = 0;
   if (!sms) {

@@ -486,8 +486,10 @@ __device__ __noinline__ int tie_select_warp(const VT* tile, int n, Scratch& sc, 
 // uniform tie-breaking in row order.  Writes sc.sperm.
 template <typename VT, int G, int NW, typename Scratch>
 __device__ __noinline__ void agg_pick_column(const VT* tile, int n, Scratch& sc, RowSet<NW> rf,
-                                             DrawRow dr, int cursor, int tid, int lane) {
+                                             DrawKey dk, int cursor, int tid, int lane) {
   constexpr int NT = 32 * G;
+  DrawCache dr;
+  dr.init(dk);
   GroupSync<G>::sync();
   for (int i = tid; i < n; i += NT) sc.sorder[i] = i;
   GroupSync<G>::sync();
@@ -1214,12 +1216,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
     }
 
     QSB_COUNT(0, 1);
-    DrawRow dr;
+    DrawKey dr;
     dr.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
     dr.seed = a.seed;
     dr.word1 = word1;
     dr.base = (uint64_t)(a.p0 + p) * (uint64_t)row_w;
-    dr.cached = ~0ULL;
 
     // ---- per-column registers.  Every global load of the particle's
     // column data is issued first; the draw block (a dependent Philox chain)
@@ -1275,8 +1276,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
         const double* cf = K::STAGE ? s_coef : a.coef + 2 * p;
         c2r2 = cf[0]; c3r3 = cf[1];
       } else {
-        c2r2 = __dmul_rn(a.c2, dr.at(0));   // engine.py:198-199: c2 * r2, c3 * r3
-        c3r3 = __dmul_rn(a.c3, dr.at(1));
+        c2r2 = __dmul_rn(a.c2, draw_at(dr, 0));   // engine.py:198-199: c2 * r2, c3 * r3
+        c3r3 = __dmul_rn(a.c3, draw_at(dr, 1));
       }
     }
 #pragma unroll
@@ -1734,7 +1735,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                     cursor += nbulk - bulk_distinct(sc, nbulk, lane);
                     nbulk = 0;
                   }
-                  const double u = dr.at(cursor++);
+                  const double u = draw_at(dr, cursor++);
                   const long long pk = (long long)__dmul_rn(u, (double)cnt);
                   src = nth_set_bit32(tb, (int)(pk >= cnt ? cnt - 1 : pk));
                   QSB_COUNT(4, 1);
@@ -1895,7 +1896,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 else cursor += nbulk - bulk_distinct_group<G>(sc, nbulk, tid, lane);
                 nbulk = 0;
               }
-              const double u = dr.at(cursor++);
+              const double u = draw_at(dr, cursor++);
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
               QSB_COUNT(4, 1);

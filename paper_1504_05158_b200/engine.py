@@ -39,19 +39,9 @@ from .instance import device_format, is_integral
 from .migration import MigrationEvent, SwarmBestTable
 from .stats import PERCENTILE_RANKS, IterationStats, _ranks_sorted, collect
 
-PHASE_INIT, PHASE_STEP, PHASE_HOST = 1, 2, 3
-_ITER_LIMIT = 1 << 32
-_PARTICLE_LIMIT = 1 << 24
+from .streams import PHASE_HOST, PHASE_INIT, PHASE_STEP, _ITER_LIMIT, _PARTICLE_LIMIT, phase_rng  # noqa: F401
+
 _LOG_EPOCHS = 256
-
-
-def phase_rng(seed: int, phase: int, iteration: int) -> np.random.Generator:
-    """numpy Philox keyed (seed, phase << 56 | iteration << 24) -- the
-    reference's stream contract (streams.py:30-40)."""
-    if not 0 <= iteration < _ITER_LIMIT:
-        raise ValueError(f"iteration {iteration} outside supported range")
-    key = np.array([int(seed) & (2**64 - 1), (phase << 56) | (iteration << 24)], dtype=np.uint64)
-    return np.random.Generator(np.random.Philox(key=key))
 
 
 def projected_buffer_bytes(config: SolverConfig, n: int) -> int:

@@ -229,7 +229,9 @@ def test_ctypes_struct_layouts_match_header():
     if cc is None:
         pytest.skip("no C compiler")
     structs = {"qsb_state": _lib.QsbState, "qsb_instance": _lib.QsbInstance,
-               "qsb_coeffs": _lib.QsbCoeffs, "qsb_migration": _lib.QsbMigration}
+               "qsb_coeffs": _lib.QsbCoeffs, "qsb_migration": _lib.QsbMigration,
+               "qsb_host_population": _lib.QsbHostPopulation,
+               "qsb_host_instance": _lib.QsbHostInstance}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "qapswarm_b200.h"',
              "int main(void) {"]
     for cname, py in structs.items():
