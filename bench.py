@@ -502,7 +502,14 @@ def main():
     if flags is not None:
         B = (2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
              + (8 * args.n if (sv == 4 and args.n > 64) else 0))   # deferred column scales
-    per_launch = B * state.local_particles
+    moved_per_launch = B * state.local_particles
+    # roofline.achieved uses SURVEY.md §8(d)'s algorithmic bytes of the
+    # velocity/normalise phase, B_vel = 2 n^2 s_V + 2 n 2 + 2 n / S per
+    # particle-iteration (read + write V, X and PL perms, PG amortised); the
+    # bytes this layout actually has to move (lazy column scale: the tile
+    # read, <= 3n entries written, column state) are reported beside it
+    B_vel = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size
+    per_launch = B_vel * state.local_particles if flags is None else moved_per_launch
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
     if pk.exists():
@@ -516,6 +523,10 @@ def main():
                 "kernel": "coef_kernel + step_kernel (draw pre-pass; fused velocity+aggregation+goal+pbest)" if flags is None
                           else "step_kernel velocity-only build",
                 "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
+                "algorithmic_bytes_per_particle": "SURVEY §8(d) B_vel = 2 n^2 s_V + 4 n + 2 n / S"
+                                                  if flags is None else "velocity-only build: V read + write",
+                "moved_bytes_per_launch": moved_per_launch,
+                "moved_frac": (moved_per_launch / (kern_max / 1000.0) / 1e9 / peak) if kern_max else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback"}
 
     # ---- the 2-opt kernel's tensor-core roofline (configs with 2-opt):
@@ -604,7 +615,7 @@ def main():
                "how": "host.step_host -> qsb_step_host (include/qapswarm_b200.h): one reference "
                       "engine.step on the reference's host PopulationState (pinned numpy buffers: "
                       "f64 V, int8 X/X_new/PL and swarm-best matrices, int64 perms/costs); every "
-                      "step copies the state host->device and the results device->host (8 "
+                      "step copies the state host->device and the results device->host (16 "
                       "swarm-aligned chunks, copies overlapped with the fused fp64 step, "
                       "migration on the device); wall clock, synchronous calls; fp64 reference "
                       "arithmetic (the host layout is the reference's float64 state)"}

@@ -99,7 +99,7 @@ Ctx& ctx() {
 
 int chunks_wanted() {
   const char* e = std::getenv("QSB_HOST_CHUNKS");
-  int k = e ? std::atoi(e) : 8;
+  int k = e ? std::atoi(e) : 16;   // 16: best of 8 / 16 / 32 / 64 at config 3 (profiles/r02/host_e2e_sweep.json)
   if (k < 1) k = 1;
   if (k > MAX_CHUNKS) k = MAX_CHUNKS;
   return k;

@@ -513,7 +513,8 @@ def _migrate_device(state: PopulationState, config: SolverConfig, t: int, exchan
         _lib.call("qsb_migrate", state.c_state(), mig, state.stream())
     else:
         exchange(state, mig)
-    state._mig.pending += 1
+    if getattr(exchange, "logs_events", True):
+        state._mig.pending += 1
 
 
 # ------------------------------------------------------------ statistics
@@ -681,7 +682,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
         d = config.migration_depth if config.migration_factor > 0.0 else 0
         # rt: the runtime object itself (its device instance is captured)
         key = (rt, hints, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr(),
-               exchange is None)
+               exchange)
         cached = getattr(state, "_graph_cache", None)
         mig = None
         if d > 0:
@@ -737,7 +738,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
         state.launches += reps * span * (3 + (1 if passes else 0)) \
             + epochs * (1 if exchange is None else 2)
         state.t += reps * span
-        if state._mig is not None:
+        if state._mig is not None and getattr(exchange, "logs_events", True):
             state._mig.pending += epochs
         state.v_bound = _post_step_v_bound(coeffs)
         state._host_best = None

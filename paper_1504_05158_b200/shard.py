@@ -86,6 +86,85 @@ def make_exchange(world: int, group=None):
     return exchange
 
 
+_RING_SEED_STRIDE = 0x9E3779B97F4A7C15   # golden-ratio odd constant: rank r's picks key
+
+
+def ring_depth(config, world: int) -> int:
+    """Donors every rank sends per ring epoch: int(f * floor(m / world)),
+    the reference's depth rule (engine.py:66-68) over the smallest shard, so
+    every rank sends and receives the same number of records."""
+    return int(config.migration_factor * (config.swarms // world))
+
+
+def make_ring_exchange(world: int, rank: int, config, group=None):
+    """Ring migration (north_star: "ring-exchanges best particles"; SURVEY
+    §8(e) optional mode, NOT the reference's semantics).
+
+    At every migration epoch rank g ranks its OWN swarms by swarm-best cost
+    (stable, as migration.py:64), picks a random current particle of each of
+    its d_g = int(f * m_g) best swarms (the reference's donor rule,
+    migration.py:74-80, with the picks stream keyed by (seed + g * c, t)),
+    sends those d records to rank g+1 and writes the d records it
+    receives from rank g-1 into its own d worst swarm bests (k-th best
+    donor -> k-th worst swarm, worse values accepted as in the reference).
+    Only the donor records (d x (n + 1) int64) cross the ring: one NCCL
+    send/recv pair per epoch instead of the all-gather + all-reduce of the
+    rank-based scheme.  With world == 1 the ring closes on the rank itself
+    and the epoch is exactly the reference migration (same seed, same d).
+
+    The donor kernel is qsb_migrate on a rank-local view of the state
+    (swarm offset 0, m = m_local): mode 1 plans and packs, the records move
+    over the ring, mode 2 applies them to the planned destinations.  No
+    MigrationEvent rows are logged in this mode."""
+    from . import _lib
+
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+
+    def exchange(state, mig, cstate=None):
+        cs = cstate if cstate is not None else state.c_state()
+        local = _lib.QsbState.from_buffer_copy(cs)
+        local.swarm_offset = 0
+        d = ring_depth(config, world)
+        if d == 0:
+            return
+        m = _lib.QsbMigration.from_buffer_copy(mig)
+        m.d = d
+        m.num_swarms_total = state.local_swarms
+        m.all_pg_cost = state.d_pg_cost.data_ptr()
+        m.log, m.log_rows, m.log_count = None, 0, None
+        m.seed = (int(config.seed) + rank * _RING_SEED_STRIDE) & (2**64 - 1)
+        stream = torch.cuda.current_stream(state.device).cuda_stream
+        if world == 1:
+            m.mode = 0
+            _lib.call("qsb_migrate", local, m, stream)
+            return
+        rec = state._mig.records[:d]
+        m.mode = 1
+        _lib.call("qsb_migrate", local, m, stream)
+        send_recv_ring(rec, nxt, prv, group)
+        m.mode = 2
+        _lib.call("qsb_migrate", local, m, stream)
+
+    exchange.logs_events = False
+    return exchange
+
+
+def send_recv_ring(buf: torch.Tensor, nxt: int, prv: int, group=None) -> torch.Tensor:
+    """Send ``buf`` to rank ``nxt`` and overwrite it with ``prv``'s buffer
+    (every rank sends the same d rows).  NCCL moves device tensors directly (capturable in a CUDA
+    graph); gloo, which has no device point-to-point, goes through host
+    copies."""
+    on_dev = buf.device.type == "cuda" and dist.get_backend(group) == "nccl"
+    out = buf if on_dev else buf.cpu()
+    inc = torch.empty_like(out)
+    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, out.contiguous(), nxt, group),
+                                   dist.P2POp(dist.irecv, inc, prv, group)])
+    for r in reqs:
+        r.wait()
+    buf.copy_(inc)
+    return buf
+
+
 @dataclass
 class BestRecord:
     cost: float

@@ -133,3 +133,56 @@ def test_sharded_migration_equals_single_process(swarms, S):
         p.join(timeout=240)
         assert p.exitcode == 0
     assert out[0] == (True, True) and out[1] == (True, True)
+
+
+# ------------------------------------------------------------ ring mode
+def _ring_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rows = torch.full((3, 5), 10 * rank, dtype=torch.int64) + torch.arange(5)
+        got = shard.send_recv_ring(rows.clone(), (rank + 1) % world, (rank - 1) % world)
+        prev = (rank - 1) % world
+        out[rank] = bool(torch.equal(got, torch.full((3, 5), 10 * prev, dtype=torch.int64)
+                                     + torch.arange(5)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_send_recv_moves_records_to_next_rank(world):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert all(out[r] for r in range(world))
+
+
+def test_ring_depth_and_world1_oracle_equals_reference_migration():
+    from types import SimpleNamespace
+    cfg = SimpleNamespace(migration_factor=0.33, swarms=800)
+    assert shard.ring_depth(cfg, 1) == int(0.33 * 800)
+    assert shard.ring_depth(cfg, 8) == int(0.33 * 100)
+    # one rank: the ring closes on itself and the epoch is migration.migrate
+    import paper_1504_05158_b200 as qsb
+    inst = qsb.taillard_uniform(12, seed=5)
+    kw = dict(c1=0.8, c2=0.5, c3=0.5, v_max=4.0, sv_mode="norm", sx_mode="second-target",
+              depth=2, seed=21)
+    st = orc.init_population(9, 4, 12, inst.flow, inst.distance, seed=21)
+    for _ in range(2):
+        orc.step(st, inst.flow, inst.distance, **kw)
+    ref_c, ref_p = st.pg_costs.copy(), st.pg_perms.copy()
+    d = int(0.34 * 9)
+    sh = dict(pg_costs=st.pg_costs.copy(), pg_perms=st.pg_perms.copy(), perms=st.perms,
+              cost=st.cost)
+    orc.ring_migrate([sh], d, 21, st.t, 4)
+    orc.migrate(d, st, orc.phase_rng(21, orc.PHASE_HOST, st.t), iteration=st.t)
+    assert np.array_equal(sh["pg_costs"], st.pg_costs)
+    assert np.array_equal(sh["pg_perms"], st.pg_perms)
+    assert not np.array_equal(ref_c, st.pg_costs) or not np.array_equal(ref_p, st.pg_perms)
