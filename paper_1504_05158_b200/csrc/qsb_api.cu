@@ -260,6 +260,31 @@ static int launch_twoopt_tc(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
+// 128 < n <= 256, one pass: the pipelined, warp-specialised kernel
+// (twoopt_tcp_kernel), one CTA per SM (its shared memory allows no more)
+static int launch_twoopt_tcp(TwoOptArgs t, cudaStream_t s) {
+  TwoOptTcp g{};
+  g.kb = (t.n + 31) / 32 * 32;
+  g.npad = (t.n + 15) / 16 * 16;
+  if (t.n <= 128 || t.n > 256 || t.passes != 1) return QSB_EUNSUPPORTED;
+  const size_t smem = TwoOptTcp::smem_bytes(t.n, g.kb);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, twoopt_tcp_kernel);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (smem + fa.sharedSizeBytes > smem_optin()) return QSB_EUNSUPPORTED;
+    e = cudaFuncSetAttribute(twoopt_tcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr = smem;
+  }
+  const int64_t cap = num_sms();
+  const int grid = (int)(t.P < cap ? t.P : cap);
+  if (grid <= 0) return QSB_OK;
+  twoopt_tcp_kernel<<<grid, TCP_NT, smem, s>>>(t, g);
+  return launch_status();
+}
+
 // n <= 32: four particles per CTA share one MMA batch (twoopt_tc4_kernel)
 static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
   constexpr int NT = 128;
@@ -286,21 +311,27 @@ static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
-static bool twoopt_use_dp4a() {
+// QSB_TWOOPT_KERNEL=dp4a | tc (A/B knobs): the dp4a kernel, or the
+// unpipelined tensor-core kernel for every n
+static int twoopt_knob() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("QSB_TWOOPT_KERNEL");
-    v = (e && strcmp(e, "dp4a") == 0) ? 1 : 0;
+    v = (e && strcmp(e, "dp4a") == 0) ? 1 : (e && strcmp(e, "tc") == 0) ? 2 : 0;
   }
-  return v == 1;
+  return v;
 }
+static bool twoopt_use_dp4a() { return twoopt_knob() == 1; }
 
 template <typename MT>
 static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = false) {
   if constexpr (sizeof(MT) == 2) {
     if (bytes && t.sym && t.n <= 256 && !twoopt_use_dp4a()) {
-      const int rc = t.n <= 32 ? launch_twoopt_tc4(t, s)
-                   : t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
+      int rc = QSB_EUNSUPPORTED;
+      if (t.n > 128 && t.passes == 1 && twoopt_knob() == 0) rc = launch_twoopt_tcp(t, s);
+      if (rc == QSB_EUNSUPPORTED)
+        rc = t.n <= 32 ? launch_twoopt_tc4(t, s)
+           : t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
       if (rc != QSB_EUNSUPPORTED) return rc;
     }
     if (bytes && t.sym) {

@@ -656,6 +656,342 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
 }
 
 
+// ---------------------------------------------------------------------------
+// Pipelined tensor-core 2-opt, one pass, 128 < n <= 256 (config 5).
+//
+// twoopt_tc_kernel above runs P-build -> MMA -> epilogue of one particle
+// after the other in one CTA, so the tensor core idles while the CTA builds
+// P = D[p][p] and scores the swaps, and the scalar pipes idle during the
+// MMA.  Here the roles are warp-specialised and consecutive particles
+// overlap:
+//   * 4 builder warps gather P = D[p][p] of the NEXT particle from D in
+//     shared memory into the (single) shared P buffer, with G[r][r], F_rr,
+//     P_rr per row;
+//   * one builder lane issues the particle's MMAs and then copies P into
+//     tensor memory (tcgen05.cp), so the P buffer is free for the next
+//     particle as soon as the tensor core is done with it;
+//   * 12 epilogue warps score the swaps from TMEM (H and the P copy) and F
+//     in shared memory, and apply the best move.
+// H is symmetric and only s > r is read: row tile 0 (r < 128) needs columns
+// 0..npad-1, row tile 1 (r >= 128) only columns 128..npad-1, so the MMAs are
+// M = 128 x N = npad and M = 128 x N = npad - 128 (3/4 of the full GEMM)
+// into TMEM columns [0, 2 npad - 128) <= 384; the P copy takes columns
+// 384..511 (row r at lane r mod 128, 64 columns per 128-row tile).
+// Epilogue warps are spread over the four TMEM lane quarters 4 / 3 / 3 / 2
+// because low rows have more s > r.  Bit-identical to twoopt_tc_kernel.
+// Barriers (CTA mbarriers): full[b] (builders -> MMA issuer and epilogue:
+// P, sv[b], sp[b] written), mma_done (MMA + copy commit -> epilogue, and
+// -> builders: P readable again), hfree (epilogue done with H and the P
+// copy -> next MMA), bfree[b] (epilogue done with sv[b], sp[b]).
+constexpr int TCP_NT = 512;
+constexpr int TCP_EPI = 12;          // epilogue warps
+constexpr int TCP_BLD = 4;           // builder warps: 11, 13, 14, 15 (warp 11 issues the MMAs)
+constexpr uint32_t TCP_PCOL = 384;   // TMEM column of the P copy
+
+struct TwoOptTcp {
+  int kb, npad;
+  static __host__ __device__ size_t smem_bytes(int n, int kb) {
+    return 2 * (size_t)256 * kb + align_up((size_t)n * (n + 1), 16) + 2 * 256 * 16 + 2 * 256 * 2 +
+           2 * TCP_EPI * 16;
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+
+// mbarrier wait with a deadlock guard: traps (a launch error, not a hung
+// GPU) when a phase has not completed for ~2^35 cycles
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  long long t0 = 0;
+  for (int spins = 0;; ++spins) {
+    uint32_t ok;
+    asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                 "selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    if (spins == 64) t0 = clock64();
+    else if (spins > 64 && (spins & 255) == 0 && clock64() - t0 > (1LL << 35)) __trap();
+  }
+}
+
+// 128 rows x 32 bytes of a canonical K-major operand -> TMEM lanes 0..127,
+// 8 columns
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
+}
+
+__global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs a, const TwoOptTcp g) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  const int n = a.n, kb = g.kb, npad = g.npad;
+  const size_t mb = (size_t)256 * kb;
+  const int dn = n + 1;
+  uint8_t* F8 = tsm;                                          // canonical layout, 256 rows
+  uint8_t* P8 = F8 + mb;                                      // P = D[p][p], same layout
+  uint8_t* D8 = P8 + mb;                                      // D row-major, stride n + 1, column n zero
+  int4* svb = reinterpret_cast<int4*>(D8 + align_up((size_t)n * dn, 16));   // [2][256] {G_rr, F_rr, P_rr, 0}
+  int16_t* spb = reinterpret_cast<int16_t*>(svb + 512);      // [2][256] the particle's perm
+  int64_t* redd = reinterpret_cast<int64_t*>(spb + 512);     // [2][TCP_EPI]
+  int* redq = reinterpret_cast<int*>(redd + 2 * TCP_EPI);    // [2][TCP_EPI]
+  __shared__ __align__(8) uint64_t full[2], bfree[2], mma_done, hfree;
+  __shared__ uint32_t s_tmem;
+  __shared__ unsigned s_mx[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
+  const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
+
+  // ---- prologue: zero the operands, F (canonical) and D (row-major) as bytes
+  if (tid < 2) s_mx[tid] = 0;
+  {
+    uint4* z = reinterpret_cast<uint4*>(F8);
+    const int nz = (int)(2 * mb / 16);
+    for (int i = tid; i < nz; i += TCP_NT) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  unsigned mf = 0, md = 0;
+  if ((n & 7) == 0) {
+    const int cw = n >> 3;                  // 8-entry chunks per row (16-byte loads)
+    for (int e = tid; e < n * cw; e += TCP_NT) {
+      const int r = e / cw, c = e - r * cw;
+      const uint4 f = *reinterpret_cast<const uint4*>(gF + (size_t)r * n + 8 * c);
+      const uint4 d = *reinterpret_cast<const uint4*>(gD + (size_t)r * n + 8 * c);
+      *reinterpret_cast<uint2*>(F8 + cl_off(r, 8 * c, kb)) =
+          make_uint2(__byte_perm(f.x, f.y, 0x6420), __byte_perm(f.z, f.w, 0x6420));
+      const uint32_t dl = __byte_perm(d.x, d.y, 0x6420), dh = __byte_perm(d.z, d.w, 0x6420);
+      uint8_t* drow = D8 + r * dn + 8 * c;  // stride n + 1: byte stores
+#pragma unroll
+      for (int x = 0; x < 4; ++x) { drow[x] = (uint8_t)(dl >> (8 * x)); drow[4 + x] = (uint8_t)(dh >> (8 * x)); }
+      const uint32_t fm = __vmaxu2(__vmaxu2(f.x, f.y), __vmaxu2(f.z, f.w));
+      const uint32_t dm = __vmaxu2(__vmaxu2(d.x, d.y), __vmaxu2(d.z, d.w));
+      mf = max(mf, max(fm & 0xffffu, fm >> 16));
+      md = max(md, max(dm & 0xffffu, dm >> 16));
+    }
+  } else {
+    for (int e = tid; e < n * n; e += TCP_NT) {
+      const int r = e / n, c = e - r * n;
+      F8[cl_off(r, c, kb)] = (uint8_t)gF[e];
+      D8[r * dn + c] = (uint8_t)gD[e];
+      mf = max(mf, (unsigned)gF[e]);
+      md = max(md, (unsigned)gD[e]);
+    }
+  }
+  for (int r = tid; r < n; r += TCP_NT) D8[r * dn + n] = 0;
+  mf = __reduce_max_sync(FULL, mf);
+  md = __reduce_max_sync(FULL, md);
+  if (lane == 0) { atomicMax(&s_mx[0], mf); atomicMax(&s_mx[1], md); }
+  if (tid == 0) {
+    mbar_init(&full[0], TCP_BLD); mbar_init(&full[1], TCP_BLD);
+    mbar_init(&bfree[0], TCP_EPI); mbar_init(&bfree[1], TCP_EPI);
+    mbar_init(&mma_done, 1); mbar_init(&hfree, TCP_EPI);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(&s_tmem)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async_smem();     // F8 / zeroed P (generic writes) -> tensor-core reads
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const bool narrow = (double)n * (double)s_mx[0] * (double)s_mx[1] < 268435456.0;
+  const int nch = npad >> 4;
+
+  if (warp == 11 || warp >= 13) {
+    // =========================== builders (+ the MMA issuer, warp 11 lane 0)
+    const int bt = (warp == 11 ? 0 : warp - 12) * 32 + lane;   // builder thread 0..127
+    const uint32_t sbo = (uint32_t)kb * 8;
+    const int ksteps = kb / 32;
+    const uint32_t id0 = umma_idesc_u8(128, npad), id1 = umma_idesc_u8(128, npad - 128);
+    const int nck = kb >> 4;                 // 16-byte chunks per row (<= 16)
+    const int c = bt % nck;                  // this thread's column chunk of P
+    const int rstep = TCP_BLD * 32 / nck;
+    int idx = 0;
+    for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x, ++idx) {
+      const int b = idx & 1;
+      int16_t* sp = spb + 256 * b;
+      int4* sv = svb + 256 * b;
+      if (idx >= 2) mbar_wait_guard(&bfree[b], ((idx >> 1) - 1) & 1);    // sv[b], sp[b] free
+      for (int i = bt; i < n; i += TCP_BLD * 32) sp[i] = a.perm[p * n + i];
+      if (idx >= 1) mbar_wait_guard(&mma_done, (idx - 1) & 1);          // P read by MMA + copy
+      asm volatile("bar.sync 2, %0;" :: "r"(TCP_BLD * 32) : "memory");
+      {
+        // P = D[p][p], 16 bytes per store: a thread keeps one 16-column chunk
+        // (its sp entries in registers) and walks rows; bytes >= n stay zero
+        int spc[16];
+#pragma unroll
+        for (int x = 0; x < 16; ++x) spc[x] = c * 16 + x < n ? sp[c * 16 + x] : n;   // n: the zero column
+        for (int i = bt / nck; i < n; i += rstep) {
+          const uint8_t* drow = D8 + sp[i] * dn;
+          unsigned w[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const unsigned b0 = drow[spc[4 * x]], b1 = drow[spc[4 * x + 1]];
+            const unsigned b2 = drow[spc[4 * x + 2]], b3 = drow[spc[4 * x + 3]];
+            w[x] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+          }
+          *reinterpret_cast<uint4*>(P8 + cl_off(i, c * 16, kb)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      asm volatile("bar.sync 2, %0;" :: "r"(TCP_BLD * 32) : "memory");
+      // G[r][r] (4-way byte dot products over the row's 16-byte chunks)
+      for (int rr = bt; rr < n; rr += TCP_BLD * 32) {
+        unsigned acc = 0;
+        for (int k = 0; k < kb; k += 16) {
+          const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(rr, k, kb));
+          const uint4 d = *reinterpret_cast<const uint4*>(P8 + cl_off(rr, k, kb));
+          acc = __dp4a(f.x, d.x, acc); acc = __dp4a(f.y, d.y, acc);
+          acc = __dp4a(f.z, d.z, acc); acc = __dp4a(f.w, d.w, acc);
+        }
+        sv[rr] = make_int4((int)acc, F8[cl_off(rr, rr, kb)], P8[cl_off(rr, rr, kb)], 0);
+      }
+      fence_proxy_async_smem();                    // P (generic writes) -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&full[b]);
+      if (warp == 11) {
+        if (lane == 0) {
+          mbar_wait_guard(&full[b], (idx >> 1) & 1);
+          if (idx >= 1) mbar_wait_guard(&hfree, (idx - 1) & 1);
+          tc_fence_after();
+          const uint32_t fa = smem_u32(F8), pa = smem_u32(P8);
+          // tile 0: rows 0..127 x columns 0..npad-1; tile 1: rows 128.. x columns 128..
+          for (int tt = 0; tt < 2; ++tt) {
+            const uint32_t off = (uint32_t)(tt * 16) * sbo;
+            for (int j = 0; j < 2 * ksteps; ++j) {
+              const bool lo = j < ksteps;
+              const uint32_t ko = (uint32_t)(lo ? j : j - ksteps) * 256;
+              const uint64_t ad = umma_smem_desc((lo ? fa : pa) + off + ko, 128, sbo);
+              const uint64_t bd = umma_smem_desc((lo ? pa : fa) + off + ko, 128, sbo);
+              umma_i8(tmem + (uint32_t)(tt * npad), ad, bd, tt ? id1 : id0, j > 0 ? 1u : 0u);
+            }
+            // the epilogue's copy of P: 32 bytes (8 columns) of 128 rows per copy
+            for (int k0 = 0; k0 < kb; k0 += 32)
+              tmem_cp_128x256b(tmem + TCP_PCOL + (uint32_t)(64 * tt + k0 / 4),
+                               umma_smem_desc(pa + off + (uint32_t)(k0 / 16) * 128, 128, sbo));
+          }
+          umma_commit(&mma_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // =========================== epilogue warps
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int jw = warp >> 2;               // index among this quarter's epilogue warps
+    const int Wq = q == 0 ? 4 : q == 3 ? 2 : 3;
+    const int e = warp < 11 ? warp : 11;    // epilogue index (warp 12 -> 11)
+    const int r0 = 32 * q + lane, r1 = 128 + r0;
+    const int len0 = max(0, nch - 2 * q);                                // tile-0 chunks c >= 2q
+    const int len1 = (128 + 32 * q < n) ? max(0, nch - 8 - 2 * q) : 0;   // tile-1 chunks c >= 8 + 2q
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const int qr0 = r0 * n - r0 * (r0 + 1) / 2 - r0 - 1;
+    const int qr1 = r1 * n - r1 * (r1 + 1) / 2 - r1 - 1;
+    int idx = 0;
+    for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x, ++idx) {
+      const int b = idx & 1;
+      mbar_wait_guard(&full[b], (idx >> 1) & 1);
+      mbar_wait_guard(&mma_done, idx & 1);
+      tc_fence_after();
+      const int4* sv = svb + 256 * b;
+      int bd = INT_MAX, bs = INT_MAX;                 // narrow: int32 deltas, bs = q index
+      int64_t wbd = INT64_MAX;
+      for (int k = jw; k < len0 + len1; k += Wq) {
+        const bool t1 = k >= len0;
+        const int c = t1 ? 8 + 2 * q + (k - len0) : 2 * q + k;
+        const int r = t1 ? r1 : r0;
+        uint32_t v[16], pw[4];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tl + (uint32_t)(t1 ? npad + (c - 8) * 16 : c * 16)));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(pw[0]), "=r"(pw[1]), "=r"(pw[2]), "=r"(pw[3])
+                     : "r"(tl + TCP_PCOL + (uint32_t)((t1 ? 64 : 0) + 4 * c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (r >= n) continue;
+        const int4 mine = sv[r];
+        const int gdr = mine.x, Frr = mine.y, Prr = mine.z;
+        const uint4 fr = *reinterpret_cast<const uint4*>(F8 + cl_off(r, c * 16, kb));
+        const unsigned fw[4] = {fr.x, fr.y, fr.z, fr.w};
+        const int qr = t1 ? qr1 : qr0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int s = c * 16 + j;
+          const int4 o = sv[s];
+          const int Frs = (int)__byte_perm(fw[j >> 2], 0u, 0x4440 | (j & 3));
+          const int Prs = (int)__byte_perm(pw[j >> 2], 0u, 0x4440 | (j & 3));
+          const int t = (2 * Frs - Frr - o.y) * (2 * Prs - Prr - o.z);   // |t| < 2^18
+          const bool ok = s > r && s < n;
+          if (narrow) {
+            const int dd = 2 * ((int)v[j] - gdr - o.x) + t;
+            if (ok && (dd < bd || (dd == bd && qr + s < bs))) { bd = dd; bs = qr + s; }
+          } else {
+            const int64_t dd = 2 * ((int64_t)v[j] - gdr - o.x) + t;
+            if (ok && (dd < wbd || (dd == wbd && qr + s < bs))) { wbd = dd; bs = qr + s; }
+          }
+        }
+      }
+      // H and the P copy drained: the next particle's MMAs may overwrite them
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&hfree);
+      int64_t best = bs == INT_MAX ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
+      int bq = bs;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      if (lane == 0) { redd[TCP_EPI * b + e] = best; redq[TCP_EPI * b + e] = bq; }
+      // the particle's goal and personal best, read before the barrier (one
+      // thread rewrites them after it)
+      const int64_t cost0 = a.cost[p];
+      const int64_t pl0 = a.do_pbest ? a.pl_cost[p] : 0;
+      asm volatile("bar.sync 1, %0;" :: "r"(32 * TCP_EPI) : "memory");
+      best = redd[TCP_EPI * b];
+      bq = redq[TCP_EPI * b];
+#pragma unroll 1
+      for (int w = 1; w < TCP_EPI; ++w) {
+        const int64_t ob = redd[TCP_EPI * b + w];
+        const int oq = redq[TCP_EPI * b + w];
+        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+      }
+      const bool move = bq != INT_MAX && best < 0;
+      int rs = -1, ss = -1;
+      if (move) unrank_pair(bq, n, rs, ss);
+      const int64_t cost = cost0 + (move ? best : 0);
+      const int et = 32 * e + lane;
+      const int16_t* sp = spb + 256 * b;
+      const bool imp = a.do_pbest && cost < pl0;
+      if (et < n) {
+        const int src = et == rs ? ss : (et == ss ? rs : et);
+        const int16_t val = sp[src];
+        a.perm[p * n + et] = val;
+        if (imp) a.pl_perm[p * n + et] = val;
+      }
+      if (et == 0) {
+        a.cost[p] = cost;
+        if (a.do_pbest) {
+          if (imp) a.pl_cost[p] = cost;
+          a.improved[p] = imp ? 1 : 0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&bfree[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512) : "memory");
+  }
+}
+
+
 // Small instances (n <= 32): four particles per CTA, one warp each, share
 // one MMA batch.  Rows 32 w .. 32 w + 31 of the stacked operands belong to
 // warp w's particle, so

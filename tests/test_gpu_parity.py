@@ -504,6 +504,28 @@ def test_twoopt_large_symmetric_vs_oracle(n):
     assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c)
 
 
+@pytest.mark.parametrize("n", [130, 200, 255, 256])
+def test_twoopt_pipelined_many_particles_vs_oracle(n):
+    """One 2-opt pass at 128 < n <= 256 runs the pipelined kernel
+    (twoopt_tcp_kernel): 400 particles put several particles through every
+    CTA, so both P buffers, the H hand-over and the epilogue reductions are
+    reused; byte entries up to 255 (the widest narrow deltas)."""
+    rng = np.random.default_rng(7 * n)
+    f = np.triu(rng.integers(0, 256, (n, n)), 1)
+    d = np.triu(rng.integers(0, 256, (n, n)), 1)
+    f, d = f + f.T, d + d.T
+    f = np.minimum(f, 255)
+    d = np.minimum(d, 255)
+    perms = np.array([rng.permutation(n) for _ in range(400)], dtype=np.int64)
+    costs = np.zeros(400, np.int64)
+    orc.cost_many(perms, f, d, costs)
+    a_p, a_c, b_p, b_c = perms.copy(), costs.copy(), perms.copy(), costs.copy()
+    orc.twoopt_many(a_p, f, d, a_c, 1)
+    batch.twoopt_many(b_p, f, d, b_c, 1)
+    assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c)
+    assert (a_c < costs).mean() > 0.9     # nearly every random permutation improves
+
+
 # ------------------------------------------------------------- CUDA graphs
 @pytest.mark.parametrize("kw", [dict(migration_factor=0.3, migration_period=1),
                                 dict(migration_factor=0.3, migration_period=3),
