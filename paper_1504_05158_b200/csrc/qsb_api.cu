@@ -348,6 +348,12 @@ extern "C" {
 
 int qsb_version(void) { return 10000; }
 
+#ifdef QSB_TCP_TIMING
+int qsb_debug_tcp_stamps(long long* out) {   // 64 x 10 clock64 stamps (diagnosis build only)
+  return cuda_status(cudaMemcpyFromSymbol(out, qsb_tcp_ts, sizeof(long long) * 640));
+}
+#endif
+
 const char* qsb_strerror(int code) {
   switch (code) {
     case QSB_OK: return "ok";

@@ -1076,7 +1076,12 @@ __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t 
 
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
-__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : 1))
+// Minimum resident CTAs: one-warp kernels QSB_MINB * 4 warps per SM; the
+// multi-warp groups two 8-warp fp32 CTAs (n <= 256; fp64 would spill) or five
+// 4-warp CTAs (n <= 128)
+// per SM -- without the bound ptxas spends 168 / 106 registers on them and
+// halves their occupancy (config 5's step kernel 0.62 -> 0.86 ms)
+__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : (G == 8 ? (sizeof(VT) == 8 ? 1 : 2) : 5)))
 step_kernel(const __grid_constant__ StepArgs a) {
   // GT: the particle tile stays in global memory (L1/L2-cached) instead of
   // being staged in smem -- used when an n x n tile exceeds shared memory.
@@ -1216,6 +1221,12 @@ step_kernel(const __grid_constant__ StepArgs a) {
     }
 
     QSB_COUNT(0, 1);
+    // multi-warp groups (n > 64) keep the last Philox block of the draw row
+    // in registers: their aggregation can take long runs of tie draws at
+    // consecutive cursors (one block serves four); the one-warp kernels are
+    // at the register cap and draw rarely
+    uint64_t dcb = ~0ULL;
+    PhiloxBlock dblk{};
     DrawKey dr;
     dr.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
     dr.seed = a.seed;
@@ -1896,7 +1907,19 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 else cursor += nbulk - bulk_distinct_group<G>(sc, nbulk, tid, lane);
                 nbulk = 0;
               }
-              const double u = draw_at(dr, cursor++);
+              double u;
+              if constexpr (G > 1) {
+                const int k = cursor++;
+                if (dr.inj) {
+                  u = dr.inj[k];
+                } else {
+                  const uint64_t idx = dr.base + (uint64_t)k;
+                  if ((idx >> 2) != dcb) { dblk = philox_block_call((idx >> 2) + 1, dr.seed, dr.word1); dcb = idx >> 2; }
+                  u = word_unit(dblk, (unsigned)(idx & 3));
+                }
+              } else {
+                u = draw_at(dr, cursor++);
+              }
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
               QSB_COUNT(4, 1);

@@ -683,16 +683,23 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
 // P, sv[b], sp[b] written), mma_done (MMA + copy commit -> epilogue, and
 // -> builders: P readable again), hfree (epilogue done with H and the P
 // copy -> next MMA), bfree[b] (epilogue done with sv[b], sp[b]).
-constexpr int TCP_NT = 512;
-constexpr int TCP_EPI = 12;          // epilogue warps
-constexpr int TCP_BLD = 4;           // builder warps: 11, 13, 14, 15 (warp 11 issues the MMAs)
+constexpr int TCP_NT = 768;          // 24 warps, 80 registers each
+constexpr int TCP_EPI = 16;          // epilogue warps
+constexpr int TCP_BLD = 8;           // builder warps (warp 15 issues the MMAs)
 constexpr uint32_t TCP_PCOL = 384;   // TMEM column of the P copy
+// warp w: TMEM lane quarter q = w & 3, index jq = w >> 2 within the quarter
+// (six per quarter).  The first TCP_EQ[q] of a quarter score swaps (5 / 4 /
+// 4 / 3: low rows have more s > r), the rest build: warps 15, 17 .. 23.
+__host__ __device__ constexpr int tcp_eq(int q) { return q == 0 ? 5 : q == 3 ? 3 : 4; }
 
 struct TwoOptTcp {
   int kb, npad;
+  // D row stride in bytes: an odd number of 4-byte words, so 32 consecutive
+  // D rows read at one column fall into 32 distinct banks
+  static __host__ __device__ int dstride(int n) { return (((n + 3) / 4) | 1) * 4; }
   static __host__ __device__ size_t smem_bytes(int n, int kb) {
-    return 2 * (size_t)256 * kb + align_up((size_t)n * (n + 1), 16) + 2 * 256 * 16 + 2 * 256 * 2 +
-           2 * TCP_EPI * 16;
+    return 2 * (size_t)256 * kb + align_up((size_t)n * dstride(n), 16) + 2 * 256 * 16 + 2 * 256 * 2 +
+           2 * 256 * 2 + 2 * TCP_EPI * 16;
   }
 };
 
@@ -700,18 +707,20 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
 
-// mbarrier wait with a deadlock guard: traps (a launch error, not a hung
-// GPU) when a phase has not completed for ~2^35 cycles
+// mbarrier wait that parks the warp (try_wait with a suspend-time hint, so
+// waiting warps do not steal issue slots from the working roles), with a
+// deadlock guard: a launch error (trap) instead of a hung GPU after 2^24
+// unsuccessful polls (each followed by a 64 ns sleep)
 __device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  long long t0 = 0;
-  for (int spins = 0;; ++spins) {
+#pragma unroll 1
+  for (uint32_t spins = 0;; ++spins) {
     uint32_t ok;
-    asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-                 "selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+                 "selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000u) : "memory");
     if (ok) return;
-    if (spins == 64) t0 = clock64();
-    else if (spins > 64 && (spins & 255) == 0 && clock64() - t0 > (1LL << 35)) __trap();
+    __nanosleep(64);      // a parked warp issues nothing (try_wait alone returned after ~100 cycles)
+    if (spins > (1u << 24)) __trap();
   }
 }
 
@@ -721,17 +730,27 @@ __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc)
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
 }
 
+#ifdef QSB_TCP_TIMING
+// diagnosis build: clock64 stamps of the pipeline events of CTA 0's first
+// 64 particles (read with qsb_debug_tcp_stamps)
+__device__ long long qsb_tcp_ts[64][10];
+#define TCP_TS(i, k) do { if (blockIdx.x == 0 && (i) < 64) qsb_tcp_ts[(i)][(k)] = clock64(); } while (0)
+#else
+#define TCP_TS(i, k) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs a, const TwoOptTcp g) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   const int n = a.n, kb = g.kb, npad = g.npad;
   const size_t mb = (size_t)256 * kb;
-  const int dn = n + 1;
+  const int dn = TwoOptTcp::dstride(n);
   uint8_t* F8 = tsm;                                          // canonical layout, 256 rows
   uint8_t* P8 = F8 + mb;                                      // P = D[p][p], same layout
-  uint8_t* D8 = P8 + mb;                                      // D row-major, stride n + 1, column n zero
+  uint8_t* D8 = P8 + mb;                                      // D row-major, stride dn
   int4* svb = reinterpret_cast<int4*>(D8 + align_up((size_t)n * dn, 16));   // [2][256] {G_rr, F_rr, P_rr, 0}
   int16_t* spb = reinterpret_cast<int16_t*>(svb + 512);      // [2][256] the particle's perm
-  int64_t* redd = reinterpret_cast<int64_t*>(spb + 512);     // [2][TCP_EPI]
+  int16_t* pinvb = spb + 512;                                 // [2][256] inverse perm (builders)
+  int64_t* redd = reinterpret_cast<int64_t*>(pinvb + 512);   // [2][TCP_EPI]
   int* redq = reinterpret_cast<int*>(redd + 2 * TCP_EPI);    // [2][TCP_EPI]
   __shared__ __align__(8) uint64_t full[2], bfree[2], mma_done, hfree;
   __shared__ uint32_t s_tmem;
@@ -775,7 +794,6 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
       md = max(md, (unsigned)gD[e]);
     }
   }
-  for (int r = tid; r < n; r += TCP_NT) D8[r * dn + n] = 0;
   mf = __reduce_max_sync(FULL, mf);
   md = __reduce_max_sync(FULL, md);
   if (lane == 0) { atomicMax(&s_mx[0], mf); atomicMax(&s_mx[1], md); }
@@ -798,61 +816,97 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
   const bool narrow = (double)n * (double)s_mx[0] * (double)s_mx[1] < 268435456.0;
   const int nch = npad >> 4;
 
-  if (warp == 11 || warp >= 13) {
-    // =========================== builders (+ the MMA issuer, warp 11 lane 0)
-    const int bt = (warp == 11 ? 0 : warp - 12) * 32 + lane;   // builder thread 0..127
+  if ((warp >> 2) >= tcp_eq(warp & 3)) {
+    // =========================== builders (+ the MMA issuer, warp 15 lane 0)
+    const int bt = (warp == 15 ? 0 : warp - 16) * 32 + lane;   // builder thread 0..255
     const uint32_t sbo = (uint32_t)kb * 8;
     const int ksteps = kb / 32;
     const uint32_t id0 = umma_idesc_u8(128, npad), id1 = umma_idesc_u8(128, npad - 128);
     const int nck = kb >> 4;                 // 16-byte chunks per row (<= 16)
-    const int c = bt % nck;                  // this thread's column chunk of P
-    const int rstep = TCP_BLD * 32 / nck;
     int idx = 0;
     for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x, ++idx) {
       const int b = idx & 1;
       int16_t* sp = spb + 256 * b;
+      int16_t* pinv = pinvb + 256 * b;      // double-buffered: a fast builder thread may
+                                            // start the next particle while others still read
       int4* sv = svb + 256 * b;
       if (idx >= 2) mbar_wait_guard(&bfree[b], ((idx >> 1) - 1) & 1);    // sv[b], sp[b] free
-      for (int i = bt; i < n; i += TCP_BLD * 32) sp[i] = a.perm[p * n + i];
+      for (int i = bt; i < n; i += TCP_BLD * 32) {
+        const int16_t v = a.perm[p * n + i];
+        sp[i] = v;
+        pinv[v] = (int16_t)i;
+      }
       if (idx >= 1) mbar_wait_guard(&mma_done, (idx - 1) & 1);          // P read by MMA + copy
       asm volatile("bar.sync 2, %0;" :: "r"(TCP_BLD * 32) : "memory");
+      if (bt == 0) TCP_TS(idx, 0);
+      // P[i] = D[p_i][p] built by SOURCE row: thread d owns D row d, i.e.
+      // P row i = pinv[d], and the warp's 32 consecutive D rows read column
+      // p_j in 32 distinct banks (odd word stride).  G[i][i] = F[i] . P[i]
+      // and P_ii come out of the same pass.
+      // the thread's D rows d = bt (+ 32 TCP_BLD ...), interleaved chunk by chunk
       {
-        // P = D[p][p], 16 bytes per store: a thread keeps one 16-column chunk
-        // (its sp entries in registers) and walks rows; bytes >= n stay zero
-        int spc[16];
+        constexpr int NR = (256 + TCP_BLD * 32 - 1) / (TCP_BLD * 32);
+        int dr[NR], ir[NR];
+        const uint8_t* drow[NR];
+        unsigned acc[NR], pii[NR];
 #pragma unroll
-        for (int x = 0; x < 16; ++x) spc[x] = c * 16 + x < n ? sp[c * 16 + x] : n;   // n: the zero column
-        for (int i = bt / nck; i < n; i += rstep) {
-          const uint8_t* drow = D8 + sp[i] * dn;
-          unsigned w[4];
+        for (int h = 0; h < NR; ++h) {
+          dr[h] = bt + h * TCP_BLD * 32;
+          ir[h] = dr[h] < n ? pinv[dr[h]] : 0;
+          drow[h] = D8 + (dr[h] < n ? dr[h] : 0) * dn;
+          acc[h] = 0; pii[h] = 0;
+        }
+#pragma unroll 1
+        for (int c = 0; c < nck; ++c) {
+          const uint4 i0 = *reinterpret_cast<const uint4*>(sp + 16 * c);       // p_j, j = 16c .. 16c+7
+          const uint4 i1 = *reinterpret_cast<const uint4*>(sp + 16 * c + 8);   // (broadcast loads)
+          const unsigned iw[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+          unsigned w[NR][4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
-            const unsigned b0 = drow[spc[4 * x]], b1 = drow[spc[4 * x + 1]];
-            const unsigned b2 = drow[spc[4 * x + 2]], b3 = drow[spc[4 * x + 3]];
-            w[x] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+            unsigned bb[NR][4];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              const int j = 16 * c + 4 * x + y;
+              const unsigned pj = (iw[(4 * x + y) >> 1] >> (16 * (y & 1))) & 0xffffu;
+#pragma unroll
+              for (int h = 0; h < NR; ++h) bb[h][y] = j < n ? (unsigned)drow[h][pj] : 0u;
+            }
+#pragma unroll
+            for (int h = 0; h < NR; ++h)
+              w[h][x] = __byte_perm(__byte_perm(bb[h][0], bb[h][1], 0x0040),
+                                    __byte_perm(bb[h][2], bb[h][3], 0x0040), 0x5410);
           }
-          *reinterpret_cast<uint4*>(P8 + cl_off(i, c * 16, kb)) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+          for (int h = 0; h < NR; ++h) {
+            if (dr[h] >= n) continue;
+            const int i = ir[h];
+            *reinterpret_cast<uint4*>(P8 + cl_off(i, 16 * c, kb)) = make_uint4(w[h][0], w[h][1], w[h][2], w[h][3]);
+            const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(i, 16 * c, kb));
+            acc[h] = __dp4a(f.x, w[h][0], acc[h]); acc[h] = __dp4a(f.y, w[h][1], acc[h]);
+            acc[h] = __dp4a(f.z, w[h][2], acc[h]); acc[h] = __dp4a(f.w, w[h][3], acc[h]);
+            if ((i >> 4) == c) {
+              const int o = i & 15;
+              const unsigned ww = o < 4 ? w[h][0] : o < 8 ? w[h][1] : o < 12 ? w[h][2] : w[h][3];
+              pii[h] = (ww >> (8 * (o & 3))) & 0xffu;
+            }
+          }
         }
+#pragma unroll
+        for (int h = 0; h < NR; ++h)
+          if (dr[h] < n) sv[ir[h]] = make_int4((int)acc[h], F8[cl_off(ir[h], ir[h], kb)], (int)pii[h], 0);
       }
-      asm volatile("bar.sync 2, %0;" :: "r"(TCP_BLD * 32) : "memory");
-      // G[r][r] (4-way byte dot products over the row's 16-byte chunks)
-      for (int rr = bt; rr < n; rr += TCP_BLD * 32) {
-        unsigned acc = 0;
-        for (int k = 0; k < kb; k += 16) {
-          const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(rr, k, kb));
-          const uint4 d = *reinterpret_cast<const uint4*>(P8 + cl_off(rr, k, kb));
-          acc = __dp4a(f.x, d.x, acc); acc = __dp4a(f.y, d.y, acc);
-          acc = __dp4a(f.z, d.z, acc); acc = __dp4a(f.w, d.w, acc);
-        }
-        sv[rr] = make_int4((int)acc, F8[cl_off(rr, rr, kb)], P8[cl_off(rr, rr, kb)], 0);
-      }
+      if (bt == 0) TCP_TS(idx, 1);
       fence_proxy_async_smem();                    // P (generic writes) -> tensor-core reads
       __syncwarp();
       if (lane == 0) mbar_arrive1(&full[b]);
-      if (warp == 11) {
+      if (warp == 15) {
         if (lane == 0) {
+          TCP_TS(idx, 2);
           mbar_wait_guard(&full[b], (idx >> 1) & 1);
+          TCP_TS(idx, 3);
           if (idx >= 1) mbar_wait_guard(&hfree, (idx - 1) & 1);
+          TCP_TS(idx, 4);
           tc_fence_after();
           const uint32_t fa = smem_u32(F8), pa = smem_u32(P8);
           // tile 0: rows 0..127 x columns 0..npad-1; tile 1: rows 128.. x columns 128..
@@ -871,6 +925,7 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
                                umma_smem_desc(pa + off + (uint32_t)(k0 / 16) * 128, 128, sbo));
           }
           umma_commit(&mma_done);
+          TCP_TS(idx, 5);
         }
         __syncwarp();
       }
@@ -879,8 +934,8 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
     // =========================== epilogue warps
     const int q = warp & 3;                 // TMEM lane quarter
     const int jw = warp >> 2;               // index among this quarter's epilogue warps
-    const int Wq = q == 0 ? 4 : q == 3 ? 2 : 3;
-    const int e = warp < 11 ? warp : 11;    // epilogue index (warp 12 -> 11)
+    const int Wq = tcp_eq(q);
+    const int e = warp < 15 ? warp : 15;    // epilogue index (warp 16 -> 15)
     const int r0 = 32 * q + lane, r1 = 128 + r0;
     const int len0 = max(0, nch - 2 * q);                                // tile-0 chunks c >= 2q
     const int len1 = (128 + 32 * q < n) ? max(0, nch - 8 - 2 * q) : 0;   // tile-1 chunks c >= 8 + 2q
@@ -893,14 +948,19 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
       mbar_wait_guard(&full[b], (idx >> 1) & 1);
       mbar_wait_guard(&mma_done, idx & 1);
       tc_fence_after();
+      if (lane == 0 && warp == 0) TCP_TS(idx, 6);
       const int4* sv = svb + 256 * b;
+      // a thread visits its pairs in increasing q (tile-0 row before its
+      // tile-1 row, chunks ascending), so a strict < keeps the first q of
+      // equal deltas
       int bd = INT_MAX, bs = INT_MAX;                 // narrow: int32 deltas, bs = q index
       int64_t wbd = INT64_MAX;
-      for (int k = jw; k < len0 + len1; k += Wq) {
+      // TMEM loads run one chunk ahead of the scoring (two register sets;
+      // tcgen05.wait::ld names the registers, so no use moves above it)
+      const int L = len0 + len1;
+      auto issue = [&](int k, uint32_t (&v)[16], uint32_t (&pw)[4]) {
         const bool t1 = k >= len0;
         const int c = t1 ? 8 + 2 * q + (k - len0) : 2 * q + k;
-        const int r = t1 ? r1 : r0;
-        uint32_t v[16], pw[4];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -909,8 +969,19 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(pw[0]), "=r"(pw[1]), "=r"(pw[2]), "=r"(pw[3])
                      : "r"(tl + TCP_PCOL + (uint32_t)((t1 ? 64 : 0) + 4 * c)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (r >= n) continue;
+      };
+      auto wait = [&](uint32_t (&v)[16], uint32_t (&pw)[4]) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                       "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]),
+                       "+r"(v[14]), "+r"(v[15]), "+r"(pw[0]), "+r"(pw[1]), "+r"(pw[2]), "+r"(pw[3])
+                     :: "memory");
+      };
+      auto score = [&](int k, const uint32_t (&v)[16], const uint32_t (&pw)[4]) {
+        const bool t1 = k >= len0;
+        const int c = t1 ? 8 + 2 * q + (k - len0) : 2 * q + k;
+        const int r = t1 ? r1 : r0;
+        if (r >= n) return;
         const int4 mine = sv[r];
         const int gdr = mine.x, Frr = mine.y, Prr = mine.z;
         const uint4 fr = *reinterpret_cast<const uint4*>(F8 + cl_off(r, c * 16, kb));
@@ -926,17 +997,34 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
           const bool ok = s > r && s < n;
           if (narrow) {
             const int dd = 2 * ((int)v[j] - gdr - o.x) + t;
-            if (ok && (dd < bd || (dd == bd && qr + s < bs))) { bd = dd; bs = qr + s; }
+            if (ok && dd < bd) { bd = dd; bs = qr + s; }
           } else {
             const int64_t dd = 2 * ((int64_t)v[j] - gdr - o.x) + t;
-            if (ok && (dd < wbd || (dd == wbd && qr + s < bs))) { wbd = dd; bs = qr + s; }
+            if (ok && dd < wbd) { wbd = dd; bs = qr + s; }
           }
         }
+      };
+      uint32_t va[16], pa[4], vb[16], pb[4];
+      int k = jw;
+      if (k < L) issue(k, va, pa);
+      while (k < L) {
+        wait(va, pa);
+        const int k2 = k + Wq;
+        if (k2 < L) issue(k2, vb, pb);
+        score(k, va, pa);
+        if (k2 >= L) break;
+        wait(vb, pb);
+        const int k3 = k2 + Wq;
+        if (k3 < L) issue(k3, va, pa);
+        score(k2, vb, pb);
+        k = k3;
       }
       // H and the P copy drained: the next particle's MMAs may overwrite them
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hfree);
+      if (lane == 0 && warp == 0) TCP_TS(idx, 7);
+      if (lane == 0 && warp == 3) TCP_TS(idx, 8);
       int64_t best = bs == INT_MAX ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
       int bq = bs;
 #pragma unroll
@@ -981,6 +1069,7 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive1(&bfree[b]);
+      if (lane == 0 && warp == 0) TCP_TS(idx, 9);
     }
   }
   tc_fence_before();
