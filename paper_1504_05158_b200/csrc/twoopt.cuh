@@ -1146,30 +1146,51 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
   const int r = lane;                        // this lane's facility (row)
   uint32_t phase = 0;
 
-  for (int64_t base = (int64_t)blockIdx.x * 4; base < a.P; base += (int64_t)gridDim.x * 4) {
+  // the next group's permutation entry and cost are loaded one round ahead
+  const int64_t gstride = (int64_t)gridDim.x * 4;
+  int nperm = 0;
+  int64_t ncost = 0;
+  {
+    const int64_t p0 = (int64_t)blockIdx.x * 4 + warp;
+    if (p0 < a.P) {
+      if (lane < n) nperm = a.perm[p0 * n + lane];
+      ncost = a.cost[p0];
+    }
+  }
+  for (int64_t base = (int64_t)blockIdx.x * 4; base < a.P; base += gstride) {
     const int64_t p = base + warp;
     const bool valid = p < a.P;
+    const int myperm = nperm;
+    uint64_t cost = valid ? (uint64_t)ncost : 0;
+    {
+      const int64_t pn = p + gstride;
+      if (pn < a.P) {
+        if (lane < n) nperm = a.perm[pn * n + lane];
+        ncost = a.cost[pn];
+      }
+    }
     __syncwarp();
-    sp[lane] = (valid && lane < n) ? a.perm[p * n + lane] : 0;
+    sp[lane] = myperm;
     __syncwarp();
     {
-      // row r of this particle's P: bytes j < n gathered, the rest zero
+      // row r of this particle's P: bytes j < n gathered (column index from
+      // lane j's register; j >= n and rows r >= n read D's zero column n)
       unsigned w[8];
-      const uint8_t* drow = D8 + sp[r] * dn;
+      const uint8_t* drow = D8 + (r < n ? myperm : 0) * dn;
 #pragma unroll
       for (int x = 0; x < 8; ++x) {
         unsigned b[4];
 #pragma unroll
         for (int y = 0; y < 4; ++y) {
           const int j = 4 * x + y;
-          b[y] = (valid && r < n && j < n) ? (unsigned)drow[sp[j]] : 0u;
+          const int pj = __shfl_sync(FULL, myperm, j);
+          b[y] = (unsigned)drow[(j < n && r < n) ? pj : n];
         }
         w[x] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
       }
       *reinterpret_cast<uint4*>(P8 + cl_off(32 * warp + r, 0, KB)) = make_uint4(w[0], w[1], w[2], w[3]);
       *reinterpret_cast<uint4*>(P8 + cl_off(32 * warp + r, 16, KB)) = make_uint4(w[4], w[5], w[6], w[7]);
     }
-    uint64_t cost = valid ? (uint64_t)a.cost[p] : 0;
     bool active = valid && a.passes > 0;
     for (int pass = 0; pass < a.passes; ++pass) {
       // G[r][r] and the diagonals of this lane's row
