@@ -317,7 +317,7 @@ typedef struct qsb_host_instance {
  * parity arithmetic: results are bit-identical to the reference's step.
  * migration_log (migrate_d x 6 doubles) receives the MigrationEvent fields.
  * Synchronous; the particles stream through the device in swarm-aligned
- * chunks (QSB_HOST_CHUNKS, default 8) with copies and compute overlapped. */
+ * chunks (QSB_HOST_CHUNKS, default 16) with copies and compute overlapped. */
 int qsb_step_host(qsb_host_population* hp, const qsb_host_instance* inst, const qsb_coeffs* co,
                   uint64_t t, int32_t migrate_d, double* migration_log);
 

@@ -173,3 +173,43 @@ def step_host(hp: HostPopulation, instance, config: SolverConfig) -> HostPopulat
                                                float(r[4]), float(r[5])))
     hp.t = t
     return hp
+
+
+def step_reference_state(state, instance, config) -> object:
+    """``engine.step(state, instance, config)`` for an object laid out like the
+    reference's own ``PopulationState`` (engine.py:85-124: X, X_new, V, PL,
+    perms, perms_new, pl_perms, cost, pl_cost, bests, best_perm, best_cost,
+    best_iteration, t, migration_log) -- the one-line drop-in of
+    INTEGRATION.md Level 1b.  The reference's buffers are used in place (no
+    copies on the host); the scalar best-so-far fields go through small
+    arrays and are written back, X / X_new and perms / perms_new are swapped
+    as engine.py:231-232 does."""
+    hp = object.__new__(HostPopulation)
+    hp.n, hp.swarms, hp.swarm_size = state.n, state.swarms, state.swarm_size
+    for name in ("X", "X_new", "V", "PL", "perms", "perms_new", "pl_perms", "cost", "pl_cost",
+                 "bests"):
+        setattr(hp, name, getattr(state, name))
+    ct = state.cost.dtype
+    hp.improved = getattr(state, "_b200_improved", None)
+    if hp.improved is None or hp.improved.shape[0] != state.cost.shape[0]:
+        hp.improved = np.empty(state.cost.shape[0], dtype=np.uint8)
+        try:
+            state._b200_improved = hp.improved
+        except AttributeError:
+            pass
+    hp._best_perm = np.ascontiguousarray(state.best_perm, dtype=np.int64)
+    hp._best_cost = np.array([state.best_cost], dtype=ct)
+    hp._best_iter = np.array([state.best_iteration], dtype=np.int64)
+    hp.t = state.t
+    hp.pmf_range = getattr(state, "pmf_range", (0.0, 1.0))
+    hp.migration_log = state.migration_log
+    hp._log = np.zeros((max(1, config.migration_depth), 6), dtype=np.float64)
+    step_host(hp, instance, config)
+    state.X, state.X_new = hp.X, hp.X_new
+    state.perms, state.perms_new = hp.perms, hp.perms_new
+    if state.best_perm is not hp._best_perm:
+        state.best_perm = hp._best_perm
+    state.best_cost = hp._best_cost[0].item()
+    state.best_iteration = int(hp._best_iter[0])
+    state.t = hp.t
+    return state

@@ -89,3 +89,35 @@ def test_step_host_from_device_state_continues_the_device_trajectory():
     assert np.array_equal(hp.bests.matrices, st.bests.matrices)
     assert (hp.best_cost, hp.best_iteration) == (st.best_cost, st.best_iteration)
     assert [tuple(e) for e in hp.migration_log] == [tuple(e) for e in st.migration_log[-2 * 3:]]
+
+
+def test_step_reference_state_on_reference_layout_object(golden_instances):
+    """host.step_reference_state on an object with exactly the reference's
+    PopulationState fields (engine.py:85-124), as the Level-1b drop-in binds
+    it: every field equals the oracle after every step, including the
+    scalar best record, the X / perms swaps and the migration log."""
+    from types import SimpleNamespace
+    inst = golden_instances["tai30"]
+    cfg = qsb.SolverConfig(swarms=6, swarm_size=7, seed=19, migration_factor=0.34,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    ost = orc.init_population(6, 7, inst.n, inst.flow, inst.distance, seed=19)
+    ref = SimpleNamespace(
+        X=ost.X.copy(), X_new=ost.X_new.copy(), V=ost.V.copy(), PL=ost.PL.copy(),
+        perms=ost.perms.copy(), perms_new=ost.perms_new.copy(), pl_perms=ost.pl_perms.copy(),
+        cost=ost.cost.copy(), pl_cost=ost.pl_cost.copy(),
+        bests=qsb.SwarmBestTable(matrices=ost.pg_mats.copy(), perms=ost.pg_perms.copy(),
+                                 costs=ost.pg_costs.copy()),
+        n=inst.n, num_particles=42, swarms=6, swarm_size=7, t=0,
+        best_perm=ost.best_perm.copy(), best_cost=ost.best_cost, best_iteration=0,
+        pmf_range=(0.0, 1.0), migration_log=[])
+    kw = orc.coeff_kwargs(cfg)
+    for k in range(5):
+        host.step_reference_state(ref, inst, cfg)
+        orc.step(ost, inst.flow, inst.distance, **kw)
+        for name in ("X", "V", "PL", "perms", "cost", "pl_cost", "pl_perms"):
+            assert getattr(ref, name).tobytes() == getattr(ost, name).tobytes(), (k, name)
+        assert ref.bests.matrices.tobytes() == ost.pg_mats.tobytes()
+        assert np.array_equal(ref.bests.costs, ost.pg_costs)
+        assert (ref.best_cost, ref.best_iteration, ref.t) == (ost.best_cost, ost.best_iteration, ost.t)
+        assert np.array_equal(ref.best_perm, ost.best_perm)
+    assert [tuple(e) for e in ref.migration_log] == [tuple(e) for e in ost.migration_log]
