@@ -2176,6 +2176,56 @@ step_kernel(const __grid_constant__ StepArgs a) {
         }
       }
     }
+    if constexpr (G > 1 && !kFloatMat) {
+      // The same incremental goal for multi-warp groups (n > 64): the moved
+      // facilities C are listed in shared memory, and every thread adds the
+      // terms of its own columns j over i in C (integer sums: the list order
+      // does not matter).  At n = 256 |C| is a few, against the n^2 terms of
+      // the full goal.
+      if (do_cost && a.cost_incremental && sizeof(MT) <= 2 && a.acc32 && n >= 8) {
+        bool mv[CPL];
+        if (tid == 0) sc.ssel[2] = 0;
+        Sync::sync();
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          mv[k] = col[k] < n && sc.sperm[col[k]] != sc.szr[col[k]];
+          if (mv[k]) sc.srow[atomicAdd(&sc.ssel[2], 1)] = (uint16_t)col[k];
+        }
+        Sync::sync();
+        const int kc = sc.ssel[2];
+        if (3 * kc <= n) {
+          int64_t acc = 0;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const int j = col[k];
+            if (j >= n) continue;
+            const int pjn = sc.sperm[j], pjo = sc.szr[j];
+            // symmetric F, D: an unmoved column's term for row i in C equals
+            // its row's term for column i, which then counts twice
+            const int w = (a.symmetric && !mv[k]) ? 2 : 1;
+#pragma unroll 4
+            for (int c = 0; c < kc; ++c) {
+              const int i = sc.srow[c];
+              const int pin = sc.sperm[i], pio = sc.szr[i];
+              // n max(F) max(D) < 2^32 and n >= 8: each term fits int32
+              acc += (int64_t)(w * (int)cF[i * n + j] * ((int)cD[pin * n + pjn] - (int)cD[pio * n + pjo]));
+              if (!a.symmetric && !mv[k])
+                acc += (int64_t)((int)cF[j * n + i] * ((int)cD[pjo * n + pin] - (int)cD[pjo * n + pio]));
+            }
+          }
+          int64_t delta = warp_sum_i64(acc);
+          if (lane == 0) sc.lslots[tid >> 5] = delta;
+          Sync::sync();
+          if (tid == 0) {
+            for (int w = 1; w < G; ++w) delta += sc.lslots[w];
+            int64_t* cp = reinterpret_cast<int64_t*>(a.cost);
+            ncost = (int64_t)((uint64_t)cp[p] + (uint64_t)delta);
+            cp[p] = ncost;
+          }
+          cost_done = true;
+        }
+      }
+    }
     if (do_cost && !cost_done) {
       const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane, a.acc32);
       if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
