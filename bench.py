@@ -108,25 +108,24 @@ def workload(args, n_gpus):
 
 
 def bytes_per_particle(n, S, sv, lazy=False, incremental_cost=True):
-    """Algorithmic HBM bytes of one fused step per particle-iteration.
+    """HBM bytes one fused step has to move per particle-iteration (the
+    ``moved_bytes`` beside the roofline; the roofline itself uses SURVEY
+    §8(d)'s B_vel).
 
-    Stored-v layout (fp64, or fp32 without the lazy column scale): V read +
+    Stored-v layout (fp64, or fp32 without the column state): V read +
     write (2 n^2 sV).  Lazily scaled fp32 layout: the tile is
-    read (4 n^2), only the <= 3n entries x / pl / pg touch are written (12n),
-    and the column state is read and written (2 * 20 * ceil4(n)).  Both:
+    read when it is staged in shared memory (4 n^2; n = 256 keeps it in
+    global memory and reads only the <= 3n touched entries), only the
+    touched entries are written (12n), and the column state is read and
+    written (2 * 20 * ceil4(n)); column rescans are not counted.  Both:
     perm / pl_perm read + perm_new write (6n), swarm best row amortised
     (2n/S), (c2 r2, c3 r3) written by the draw pre-pass and read (32), cost
-    read (incremental goal) and written, pl_cost read, improved flag (25).
-    fp32 with n > 64 (deferred column normalisation): V read + write and the
-    n column scales read + written."""
+    read (incremental goal) and written, pl_cost read, improved flag (25)."""
     common = 6 * n + 2 * n / S + 32 + (25 if incremental_cost else 17)
-    if lazy and n <= 64:
-        vcs = (n + 3) // 4 * 4
-        return 4 * n * n + 12 * n + 40 * vcs + common
     if lazy:
-        # n > 64, fp32: deferred column normalisation (V read + write once,
-        # the column scales read and written)
-        return 2 * n * n * sv + 8 * n + common
+        vcs = (n + 3) // 4 * 4
+        tile = 4 * n * n if 4 * n * n <= 200 * 1024 else 12 * n
+        return tile + 12 * n + 40 * vcs + common
     return 2 * n * n * sv + common
 
 
@@ -500,8 +499,7 @@ def main():
     lazy = getattr(state, "d_vcol", None) is not None
     B = bytes_per_particle(args.n, args.swarm_size, sv, lazy=lazy)
     if flags is not None:
-        B = (2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
-             + (8 * args.n if (sv == 4 and args.n > 64) else 0))   # deferred column scales
+        B = 2 * args.n * args.n * sv + 4 * args.n + 2 * args.n / args.swarm_size + 32
     moved_per_launch = B * state.local_particles
     # roofline.achieved uses SURVEY.md §8(d)'s algorithmic bytes of the
     # velocity/normalise phase, B_vel = 2 n^2 s_V + 2 n 2 + 2 n / S per

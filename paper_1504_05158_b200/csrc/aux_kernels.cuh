@@ -473,7 +473,7 @@ __global__ void perm_to_mat_kernel(const PT* perm, int64_t P, int n, int8_t* x) 
 // identity and U(-amp, amp) the same way, from its own sequential stream).
 template <typename VT>
 __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vstride, double amp,
-                            int16_t* perm, VT* V) {
+                            int16_t* perm, VT* V, int wide) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint64_t word1 = stream_word(4, 0);
@@ -489,7 +489,7 @@ __global__ void init_kernel(uint64_t seed, int64_t p0, int64_t P, int n, int vst
         // (-amp) + (2 amp) u with separate roundings (no FMA), so the oracle
         // restates it in numpy (oracle.device_init)
         const double v = __dadd_rn(-amp, __dmul_rn(__dmul_rn(2.0, amp), u));
-        if constexpr (sizeof(VT) == 4) vp[e] = n <= WIDE_MAX_N ? (VT)wenc(v) : (VT)v;
+        if constexpr (sizeof(VT) == 4) vp[e] = wide ? (VT)wenc(v) : (VT)v;
         else vp[e] = (VT)v;
       } else {
         vp[e] = (VT)0;

@@ -140,12 +140,12 @@ __device__ __forceinline__ double cell_m(VT v, bool x_one) {
 }
 
 // ------------------------------------------------ wide 32-bit velocity words
-// fp32 velocity tiles in the lazily scaled layout (n <= 64, the one-warp
-// step kernels) store the high word of the double (sign, 11-bit exponent,
-// 20-bit fraction), rounded to nearest: fp32's size with fp64's exponent
-// range (step_kernel.cuh, vval).  A state is created lazily scaled, so the
-// throughput-mode init writes these words for n <= WIDE_MAX_N.
-constexpr int WIDE_MAX_N = 64;
+// fp32 velocity tiles in the lazily scaled layout (every fp32 state with a
+// column-state array, n <= 256; step_kernel.cuh, vval) store the high word of
+// the double (sign, 11-bit exponent, 20-bit fraction), rounded to nearest:
+// fp32's size with fp64's exponent range.  The throughput-mode init writes
+// these words when the state is lazily scaled.
+constexpr int WIDE_MAX_N = 256;
 __device__ __forceinline__ double wdec(float w) { return __hiloint2double(__float_as_int(w), 0); }
 __device__ __forceinline__ float wenc(double d) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(d) + 0x80000000ULL;

@@ -78,6 +78,15 @@ static size_t smem_optin() {
   return (size_t)v;
 }
 
+// QSB_MW_DEFER=1 (A/B): fp32 states with n > 64 keep the pre-round-2
+// deferred column scale instead of the lazily scaled layout; the Python
+// engine reads the same variable (engine._LAZY_MAX_N)
+static int mw_defer() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("QSB_MW_DEFER"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v;
+}
+
 // ------------------------------------------------------------ fused step
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 static int launch_step(const StepArgs& a, cudaStream_t s) {
@@ -413,6 +422,7 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.cost_incremental = (co->hints & QSB_HINT_COST_CURRENT) ? 1 : 0;
   a.symmetric = (co->hints & QSB_HINT_SYMMETRIC) ? 1 : 0;
   a.vcol = st->v_dtype == QSB_F32 ? st->vcol : nullptr;
+  a.mw_defer = mw_defer();
   a.vcstride = (st->n + 3) / 4 * 4;
 }
 
@@ -642,14 +652,16 @@ int qsb_step_draws(uint64_t seed, uint64_t t, int64_t p0, int64_t P, int32_t n, 
 
 int qsb_init_population_device(const qsb_state* st, uint64_t seed, double amp, void* stream) {
   if (!st || !st->perm || !st->V) return QSB_EINVAL;
+  // wide words iff the state is lazily scaled (engine.PopulationState.v_wide)
+  const int wide = st->v_dtype == QSB_F32 && st->vcol && st->n <= WIDE_MAX_N && (st->n <= 64 || !mw_defer());
   const int grid = (int)((st->num_particles + 7) / 8 < 8 * num_sms() ? (st->num_particles + 7) / 8 : 8 * num_sms());
   if (grid <= 0) return QSB_OK;
   if (st->v_dtype == QSB_F32)
     init_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, st->particle_offset, st->num_particles,
-                                                                st->n, st->vstride, amp, st->perm, (float*)st->V);
+                                                                st->n, st->vstride, amp, st->perm, (float*)st->V, wide);
   else
     init_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, st->particle_offset, st->num_particles,
-                                                                 st->n, st->vstride, amp, st->perm, (double*)st->V);
+                                                                 st->n, st->vstride, amp, st->perm, (double*)st->V, 0);
   return launch_status();
 }
 

@@ -72,8 +72,10 @@ struct StepArgs {
   int cost_incremental;      // host guarantee: cost[p] == goal(perm[p]) on entry
   int symmetric;             // host guarantee: F and D symmetric (integral instances)
   unsigned int* work;        // optional zeroed counter: dynamic particle scheduling
-  float* vcol;               // fp32 lazily scaled layout: (P, 4, vcstride) column state, or null
+  float* vcol;               // fp32 lazily scaled layout: (P, 5, vcstride) column state, or null
   int vcstride;
+  int mw_defer;              // n > 64 fp32 with vcol: 1 = deferred column scale (row 0 only,
+                             // float tile; QSB_MW_DEFER=1 A/B), 0 = the lazily scaled layout
 };
 
 struct Best {
@@ -1077,11 +1079,12 @@ __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t 
 // ------------------------------------------------------------------------
 template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
 // Minimum resident CTAs: one-warp kernels QSB_MINB * 4 warps per SM; the
-// multi-warp groups two 8-warp fp32 CTAs (n <= 256; fp64 would spill) or five
+// multi-warp groups two 8-warp fp32 CTAs with the tile in global memory (n = 256;
+// fp64 would spill, smem tiles allow one CTA anyway) or five
 // 4-warp CTAs (n <= 128)
 // per SM -- without the bound ptxas spends 168 / 106 registers on them and
 // halves their occupancy (config 5's step kernel 0.62 -> 0.86 ms)
-__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : (G == 8 ? (sizeof(VT) == 8 ? 1 : 2) : 5)))
+__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : (G == 8 ? ((sizeof(VT) == 8 || !GT) ? 1 : 2) : 5)))
 step_kernel(const __grid_constant__ StepArgs a) {
   // GT: the particle tile stays in global memory (L1/L2-cached) instead of
   // being staged in smem -- used when an n x n tile exceeds shared memory.
@@ -1094,14 +1097,16 @@ step_kernel(const __grid_constant__ StepArgs a) {
   // Lazily scaled fp32 layout (a.vcol set; one-warp groups): the tile holds
   // u with v = u * s per column, and a step rewrites only the <= 3 entries
   // per column that x / pl / pg touch ("lazy column scale").
-  constexpr bool kLazy = sizeof(VT) == 4 && G == 1 && !GT;
-  const bool lazy = kLazy && a.vcol != nullptr;
+  // (multi-warp groups too, since round 2: the global-memory tile (GT)
+  // included; each thread owns one column and rescans its own column)
+  constexpr bool kLazy = sizeof(VT) == 4 && (G > 1 || !GT);
+  const bool lazy = kLazy && a.vcol != nullptr && (G == 1 || !a.mw_defer);
   const bool wide = lazy;   // lazily scaled fp32 tiles hold wide words (vval)
   // multi-warp fp32 kernels with a column-scale array: deferred column
   // normalisation -- the tile keeps the unnormalised velocity u and row 0
   // of vcol the column scale s (v = u * s), so a step reads and writes every
   // entry once, with no second (rescale) pass over the tile
-  const bool defer = sizeof(VT) == 4 && G > 1 && a.vcol != nullptr;
+  const bool defer = sizeof(VT) == 4 && G > 1 && a.vcol != nullptr && !lazy;
 
   // PDL: everything below may read what the previous kernel (coef_kernel,
   // best_kernel, migrate_kernel, 2-opt) wrote
@@ -1313,7 +1318,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
         ok &= cM[k] == cM[k] && csd[k] >= 0x1p-900 && csd[k] <= 0x1p900 && c1s >= 0x1p-900 &&
               c1s <= 0x1p900 && c1s >= (double)lb * 0x1p-900;
       }
-      incr = __all_sync(FULL, ok);
+      if constexpr (G == 1) incr = __all_sync(FULL, ok);
+      else incr = __syncthreads_and(ok);      // one group per CTA (W = 1)
       if (!incr) QSB_COUNT(8, 1);
     }
 
@@ -1403,7 +1409,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           double Ad = cA[k];
           bool bad = false;
           float* colp = reinterpret_cast<float*>(tile) + col[k];
-          float* gcol = reinterpret_cast<float*>(gV) + col[k];
+          float* gcol = reinterpret_cast<float*>(gV) + col[k];   // == colp for GT tiles
           // the touched rows and their pulls c2 r2 (pl - x) + c3 r3 (pg - x):
           //   x row: -c2 r2 [x != pl] - c3 r3 [x != pg] (none: unchanged)
           //   pl row (!= x): c2 r2 + c3 r3 [pl == pg];  pg row (!= x, pl): c3 r3
@@ -1416,7 +1422,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
             const double u2d = (double)lin * rcd;
             const float u2 = wenc(u2d);
             colp[r * n] = u2;
-            if (store_v) gcol[r * n] = u2;
+            if (store_v && !GT) gcol[r * n] = u2;
             Ad += fabs(wdec(u2)) - fabs(ud);
             if (r == zp) return;
             if (u2 > M) { M = u2; cnt = 1; R = r; }
@@ -1510,6 +1516,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
             nmax[k] = cM[k]; ncnt[k] = cCR[k] >> 16; nrow[k] = (cCR[k] >> 8) & 0xff;
           }
         }
+        if constexpr (G == 1) {
         // cooperative rescans (lanes over rows): non-z max / count / first
         // row, and the sum of |u| over all rows
 #pragma unroll
@@ -1554,6 +1561,56 @@ step_kernel(const __grid_constant__ StepArgs a) {
               cA[k] = sum;
               cM[k] = (float)nmax[k];
               cCR[k] = tot ? (((int)tot << 16) | ((int)rr << 8) | zc) : -1;
+            }
+          }
+        }
+        } else {
+          // multi-warp groups: each warp rescans the columns it owns, lanes
+          // over rows (rows lane + 32 j), warp reductions only -- no group
+          // barrier; the columns of a group are independent
+          constexpr int RPL = (K::NMAX + 31) / 32;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            unsigned mask = __ballot_sync(FULL, need[k]);
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              mask &= mask - 1;
+              QSB_COUNT(9, 1);
+              const int c = __shfl_sync(FULL, col[k], src);
+              const int zc = __shfl_sync(FULL, zr[k], src);
+              const float* colq = reinterpret_cast<const float*>(tile) + c;
+              unsigned kj[RPL];
+              unsigned km = 0;
+              double sum = 0.0;
+#pragma unroll
+              for (int j = 0; j < RPL; ++j) {
+                const int r = lane + 32 * j;
+                kj[j] = 0u;
+                if (r >= n) continue;
+                const float u = colq[r * n];   // wide word
+                sum += fabs(wdec(u));
+                if (r == zc) continue;
+                kj[j] = okey32(__fadd_rn(u, 0.0f));
+                km = max(km, kj[j]);
+              }
+              const unsigned M = __reduce_max_sync(FULL, km);
+              unsigned tot = 0, rr = INT_MAX;
+#pragma unroll
+              for (int j = RPL - 1; j >= 0; --j) {
+                const unsigned bb = __ballot_sync(FULL, M != 0u && kj[j] == M);
+                tot += __popc(bb);
+                if (bb) rr = j * 32 + __ffs(bb) - 1;
+              }
+#pragma unroll
+              for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+              if (lane == src) {
+                ncnt[k] = (int)tot;
+                nrow[k] = tot ? (int)rr : -1;
+                nmax[k] = tot ? (VT)from_okey32(M) : (VT)0;
+                cA[k] = sum;
+                cM[k] = (float)nmax[k];
+                cCR[k] = tot ? (((int)tot << 16) | ((int)rr << 8) | zc) : -1;
+              }
             }
           }
         }
@@ -2091,7 +2148,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                   ncnt[k] = rr.cnt;
                   nrow[k] = rr.cnt ? rr.col : -1;
                   nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
-                  nk64[k] = rr.cnt ? nonz_key(nmax[k], sc.sS[c], false) : 0;
+                  nk64[k] = rr.cnt ? nonz_key(nmax[k], sc.sS[c], sc.wide) : 0;
                   recompute(k);
                 }
             }

@@ -55,7 +55,11 @@ def projected_buffer_bytes(config: SolverConfig, n: int) -> int:
     return mats + perms + tables + swarm
 
 
-_LAZY_MAX_N = 64      # one-warp kernel variants carry the lazily scaled layout
+# fp32 states up to this n carry the lazily scaled layout (wide words, five
+# column-state rows); the one-warp kernels since round 1, the multi-warp
+# kernels (n <= 256) since round 2.  QSB_MW_DEFER=1 keeps n > 64 on the
+# deferred column scale (A/B; read by libqsb too).
+_LAZY_MAX_N = 64 if _os.environ.get("QSB_MW_DEFER", "") == "1" else 256
 
 
 def _vcs(n: int) -> int:

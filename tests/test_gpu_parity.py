@@ -284,7 +284,7 @@ def test_fp32_lazy_layout_matrix(n, coef):
         qsb.step(st, inst, cfg)
     perms = st.perms
     assert (np.sort(perms, axis=1) == np.arange(n)).all(), "positions must stay permutations"
-    if st.d_vcol is not None and n <= 64:
+    if st.v_wide:
         _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
     ost = orc.init_population(6, 20, n, inst.flow, inst.distance, seed=n)
     ost.X, ost.perms = st.X, st.perms
@@ -310,7 +310,7 @@ def test_fp32_lazy_layout_matrix(n, coef):
     cost = np.zeros(cfg.num_particles, np.int64)
     orc.cost_many(out_perm, inst.flow, inst.distance, cost)
     assert np.array_equal(cost, st.cost)
-    if st.d_vcol is not None and n <= 64:
+    if st.v_wide:
         _lazy_state_checks(st, n, normalised=cf.sv_mode == "norm")
 
 
