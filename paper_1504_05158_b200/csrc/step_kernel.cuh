@@ -1141,7 +1141,17 @@ step_kernel(const __grid_constant__ StepArgs a) {
     const MT* gF = reinterpret_cast<const MT*>(a.F);
     const MT* gD = reinterpret_cast<const MT*>(a.D);
     if (G == 1 || fds) {
-      for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
+      if ((nn * sizeof(MT)) % 16 == 0) {
+        // 16-byte copies (sD = sF + nn stays aligned)
+        const int nv = (int)(nn * sizeof(MT) / 16);
+        const uint4* gF4 = reinterpret_cast<const uint4*>(gF);
+        const uint4* gD4 = reinterpret_cast<const uint4*>(gD);
+        uint4* sF4 = reinterpret_cast<uint4*>(sF);
+        uint4* sD4 = reinterpret_cast<uint4*>(sD);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) { sF4[i] = gF4[i]; sD4[i] = gD4[i]; }
+      } else {
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
+      }
     } else {
       cF = gF; cD = gD;
     }
@@ -1891,12 +1901,23 @@ step_kernel(const __grid_constant__ StepArgs a) {
               if (tid == 0) sc.ssel[2] = 0;
               if (tid < NW) sc.rmw[tid] = 0ULL;
               __syncthreads();
+              // warp-aggregated: one position atomic and one OR per row word
+              // per warp (the order of the bulk keys does not matter)
 #pragma unroll
               for (int k = 0; k < CPL; ++k) {
-                if (!q[k]) continue;
-                const int pos = atomicAdd(&sc.ssel[2], 1);
-                sc.sbulk[nbulk + pos] = zkey[k];
-                atomicOr(&sc.rmw[zr[k] >> 6], 1ULL << (zr[k] & 63));
+                const unsigned qb = __ballot_sync(FULL, q[k]);
+                if (!qb) continue;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&sc.ssel[2], __popc(qb));
+                base = __shfl_sync(FULL, base, 0);
+                if (q[k]) sc.sbulk[nbulk + base + __popc(qb & ((1u << lane) - 1u))] = zkey[k];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                  const uint64_t bit = (q[k] && (zr[k] >> 6) == w) ? 1ULL << (zr[k] & 63) : 0ULL;
+                  const unsigned lo = __reduce_or_sync(FULL, (unsigned)bit);
+                  const unsigned hi = __reduce_or_sync(FULL, (unsigned)(bit >> 32));
+                  if (lane == 0 && (lo | hi)) atomicOr(&sc.rmw[w], ((unsigned long long)hi << 32) | lo);
+                }
               }
               __syncthreads();
               const int nq = sc.ssel[2];
@@ -2119,40 +2140,41 @@ step_kernel(const __grid_constant__ StepArgs a) {
               }
             }
           } else {
-            if (tid == 0) sc.ssel[2] = 0;
-            __syncthreads();
+            // multi-warp groups: each warp rescans the columns it owns,
+            // lanes over rows, warp reductions only (no group barrier; the
+            // columns of a group are independent)
+            constexpr int RPL = (K::NMAX + 31) / 32;
 #pragma unroll
-            for (int k = 0; k < CPL; ++k)
-              if (need[k]) sc.srow[atomicAdd(&sc.ssel[2], 1)] = col[k];
-            __syncthreads();
-            const int cnt = sc.ssel[2];
-            for (int i = 0; i < cnt; ++i) {
-              const int c = sc.srow[i];
-              const int zc = sc.szr[c];
-              Best rb = best_none();
+            for (int k = 0; k < CPL; ++k) {
+              unsigned mask = __ballot_sync(FULL, need[k]);
+              while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                QSB_COUNT(7, 1);
+                const int c = __shfl_sync(FULL, col[k], src);
+                const int zc = __shfl_sync(FULL, zr[k], src);
+                Best rb = best_none();
 #pragma unroll
-              for (int j = 0; j < CPL; ++j) {
-                const int r = tid + j * NT;
-                if (r >= n || r == zc || !rf.has(r)) continue;
-                // ordered by the stored value (the column scale is positive
-                // and u * s is exact in double, so the order and the ties
-                // are those of v); nmax keeps the stored value
-                const uint64_t key = nonz_key(tile[r * n + c], 1.0f, false);
-                if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
-                else if (key == rb.key) ++rb.cnt;
-              }
-              const Best rr = group_best<G>(rb, sc, par, lane, tid);
-#pragma unroll
-              for (int k = 0; k < CPL; ++k)
-                if (col[k] == c) {
+                for (int j = 0; j < RPL; ++j) {
+                  const int r = lane + 32 * j;
+                  if (r >= n || r == zc || !rf.has(r)) continue;
+                  // ordered by the stored value (the column scale is positive
+                  // and u * s is exact in double, so the order and the ties
+                  // are those of v); nmax keeps the stored value
+                  const uint64_t key = nonz_key(tile[r * n + c], 1.0f, false);
+                  if (key > rb.key) { rb.key = key; rb.cnt = 1; rb.col = r; }
+                  else if (key == rb.key) ++rb.cnt;
+                }
+                const Best rr = warp_best(rb);
+                if (lane == src) {
                   ncnt[k] = rr.cnt;
                   nrow[k] = rr.cnt ? rr.col : -1;
                   nmax[k] = rr.cnt ? (VT)from_okey(rr.key) : (VT)0;
                   nk64[k] = rr.cnt ? nonz_key(nmax[k], sc.sS[c], sc.wide) : 0;
                   recompute(k);
                 }
+              }
             }
-            __syncthreads();
           }
         }
       }
