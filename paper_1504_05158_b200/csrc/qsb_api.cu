@@ -27,15 +27,23 @@ static int launch_status() { return cuda_status(cudaGetLastError()); }
 // CUDA errors of the other translation unit (host_step.cu)
 void qsb_note_cuda_error(int e) { g_last_cuda = e; }
 
+// Launch-time caches (SM counts, shared-memory limits, function attributes,
+// occupancy) are kept per device, so one process may drive several GPUs.
+constexpr int MAX_DEV = 64;
+static int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= MAX_DEV ? MAX_DEV - 1 : d);
+}
+
 static int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[MAX_DEV] = {};
+  const int d = cur_dev();
+  if (!sms[d]) {
+    cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+    if (sms[d] <= 0) sms[d] = 148;
   }
-  return sms;
+  return sms[d];
 }
 
 // Launch with programmatic stream serialization (PDL) so the kernel's launch
@@ -68,14 +76,13 @@ static int launch_pdl(void (*fn)(KArgs...), int grid, int block, size_t smem, cu
 }
 
 static size_t smem_optin() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (v <= 0) v = 227 * 1024;
+  static int v[MAX_DEV] = {};
+  const int d = cur_dev();
+  if (!v[d]) {
+    cudaDeviceGetAttribute(&v[d], cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    if (v[d] <= 0) v[d] = 227 * 1024;
   }
-  return (size_t)v;
+  return (size_t)v[d];
 }
 
 // QSB_MW_DEFER=1 (A/B): fp32 states with n > 64 keep the pre-round-2
@@ -97,24 +104,25 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
   auto fn = step_kernel<VT, MT, G, CPL, W, GT>;
-  static size_t attr_smem = 0;
-  static size_t occ_smem = 0;
-  static int occ_blocks = 0;
-  if (smem > attr_smem) {
+  static size_t attr_smem[MAX_DEV] = {};
+  static size_t occ_smem[MAX_DEV] = {};
+  static int occ_blocks[MAX_DEV] = {};
+  const int d = cur_dev();
+  if (smem > attr_smem[d]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_status(e);
-    attr_smem = smem;
+    attr_smem[d] = smem;
   }
-  if (occ_smem != smem) {
+  if (occ_smem[d] != smem) {
     int bps = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 32 * G * W, smem);
     if (e != cudaSuccess) return cuda_status(e);
-    occ_blocks = bps > 0 ? bps : 1;
-    occ_smem = smem;
+    occ_blocks[d] = bps > 0 ? bps : 1;
+    occ_smem[d] = smem;
   }
   if (a.P <= 0) return QSB_OK;
   const int64_t want = (a.P + W - 1) / W;
-  const int64_t cap = (int64_t)num_sms() * occ_blocks;
+  const int64_t cap = (int64_t)num_sms() * occ_blocks[d];
   const int grid = (int)(want < cap ? want : cap);
   return launch_pdl(fn, grid, 32 * G * W, smem, s, b);
 }
@@ -236,7 +244,8 @@ static int launch_twoopt_tc(TwoOptArgs t, cudaStream_t s) {
   g.tcols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   if (g.tiles > 2 || (g.tiles == 2 && NT != 256)) return QSB_EUNSUPPORTED;
   auto fn = twoopt_tc_kernel<NT>;
-  static size_t dyn_max = 0;
+  static size_t dyn_max_dev[MAX_DEV] = {};
+  size_t& dyn_max = dyn_max_dev[cur_dev()];
   if (!dyn_max) {
     cudaFuncAttributes fa{};
     cudaError_t e = cudaFuncGetAttributes(&fa, fn);
@@ -277,7 +286,8 @@ static int launch_twoopt_tcp(TwoOptArgs t, cudaStream_t s) {
   g.npad = (t.n + 15) / 16 * 16;
   if (t.n <= 128 || t.n > 256 || t.passes != 1) return QSB_EUNSUPPORTED;
   const size_t smem = TwoOptTcp::smem_bytes(t.n, g.kb);
-  static size_t attr = 0;
+  static size_t attr_dev[MAX_DEV] = {};
+  size_t& attr = attr_dev[cur_dev()];
   if (smem > attr) {
     cudaFuncAttributes fa{};
     cudaError_t e = cudaFuncGetAttributes(&fa, twoopt_tcp_kernel);
