@@ -100,7 +100,11 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   using K = StepKernel<VT, MT, G, CPL, W, GT>;
   StepArgs b = a;
   const bool need_fd = (a.flags & F_COST) != 0;
-  b.fd_smem = need_fd && (G == 1 || K::smem_bytes(a.n, a.vstride, true) <= smem_optin());
+  // one-warp kernels stage F and D once per SM (one 16-warp CTA); the
+  // multi-warp groups (one particle per CTA, several CTAs per SM) read them
+  // through L1 when the goal is incremental (a few rows per step) instead of
+  // spending shared memory -- and CTAs per SM -- on a copy per CTA
+  b.fd_smem = need_fd && (G == 1 || (!a.cost_incremental && K::smem_bytes(a.n, a.vstride, true) <= smem_optin()));
   const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
   auto fn = step_kernel<VT, MT, G, CPL, W, GT>;
