@@ -1242,11 +1242,17 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // at the register cap and draw rarely
     uint64_t dcb = ~0ULL;
     PhiloxBlock dblk{};
-    DrawKey dr;
-    dr.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
-    dr.seed = a.seed;
-    dr.word1 = word1;
-    dr.base = (uint64_t)(a.p0 + p) * (uint64_t)row_w;
+    // the particle's draw row, built where a draw is taken (ties, pick-
+    // column, no pre-pass): the key is kernel constants plus p, so it needs
+    // no registers across the particle
+    auto mkdr = [&]() -> DrawKey {
+      DrawKey d;
+      d.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
+      d.seed = a.seed;
+      d.word1 = word1;
+      d.base = (uint64_t)(a.p0 + p) * (uint64_t)row_w;
+      return d;
+    };
 
     // ---- per-column registers.  Every global load of the particle's
     // column data is issued first; the draw block (a dependent Philox chain)
@@ -1302,8 +1308,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
         const double* cf = K::STAGE ? s_coef : a.coef + 2 * p;
         c2r2 = cf[0]; c3r3 = cf[1];
       } else {
-        c2r2 = __dmul_rn(a.c2, draw_at(dr, 0));   // engine.py:198-199: c2 * r2, c3 * r3
-        c3r3 = __dmul_rn(a.c3, draw_at(dr, 1));
+        c2r2 = __dmul_rn(a.c2, draw_at(mkdr(), 0));   // engine.py:198-199: c2 * r2, c3 * r3
+        c3r3 = __dmul_rn(a.c3, draw_at(mkdr(), 1));
       }
     }
 #pragma unroll
@@ -1734,7 +1740,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       int cursor = a.agg_base;     // next aggregation draw (column in the draw row)
 
       if (a.mode == MODE_PICK_COLUMN) {
-        agg_pick_column<VT, G, NW>(tile, n, sc, rf, dr, cursor, tid, lane);
+        agg_pick_column<VT, G, NW>(tile, n, sc, rf, mkdr(), cursor, tid, lane);
       } else {
         bool restricted = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
         // cached per-column candidate: (key, tie count, first row) of the
@@ -1813,7 +1819,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                     cursor += nbulk - bulk_distinct(sc, nbulk, lane);
                     nbulk = 0;
                   }
-                  const double u = draw_at(dr, cursor++);
+                  const double u = draw_at(mkdr(), cursor++);
                   const long long pk = (long long)__dmul_rn(u, (double)cnt);
                   src = nth_set_bit32(tb, (int)(pk >= cnt ? cnt - 1 : pk));
                   QSB_COUNT(4, 1);
@@ -1988,6 +1994,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
               double u;
               if constexpr (G > 1) {
                 const int k = cursor++;
+                const DrawKey dr = mkdr();
                 if (dr.inj) {
                   u = dr.inj[k];
                 } else {
@@ -1996,7 +2003,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                   u = word_unit(dblk, (unsigned)(idx & 3));
                 }
               } else {
-                u = draw_at(dr, cursor++);
+                u = draw_at(mkdr(), cursor++);
               }
               const long long pk = (long long)__dmul_rn(u, (double)b.cnt);
               const int pick = (int)(pk >= b.cnt ? b.cnt - 1 : pk);
