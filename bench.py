@@ -307,6 +307,24 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------- main
+def preload_kernels(cfg, inst, dev):
+    """Launch every kernel a timed step can launch once, on a throwaway
+    16-particle population of the same n / precision / 2-opt setting with
+    migration every iteration, so that CUDA's lazy module loading happens
+    here and not at the first migration epoch inside a timed window (the
+    warmup steps alone never reach t = migration_period)."""
+    import dataclasses
+    import torch
+    import paper_1504_05158_b200 as qsb
+    small = dataclasses.replace(cfg, swarms=4, swarm_size=4, migration_period=1,
+                                migration_factor=max(cfg.migration_factor, 0.25))
+    st = qsb.init_population(small, inst, device=dev)
+    for _ in range(3):
+        qsb.step(st, inst, small)
+    torch.cuda.synchronize()
+    del st
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -338,6 +356,7 @@ def main():
             dist.init_process_group(backend)
     inst = qsb.taillard_uniform(args.n)
     cfg = config(args)
+    preload_kernels(cfg, inst, dev)
     lo, hi = shard.swarm_range(cfg.swarms, world, rank)
     state = qsb.init_population(cfg, inst, device=dev, swarm_range=(lo, hi))
     exchange = shard.make_exchange(world) if world > 1 else None

@@ -10,6 +10,7 @@
 #include "aux_kernels.cuh"
 #include "step_kernel.cuh"
 #include "twoopt.cuh"
+#include "twoopt_pair.cuh"
 #include "stats.cuh"
 
 using namespace qsb;
@@ -308,6 +309,31 @@ static int launch_twoopt_tcp(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
+// 128 < n <= 256, one pass, QSB_TWOOPT_KERNEL=pair: the CTA-pair kernel
+// (twoopt_pair.cuh), one pair per two SMs
+static int launch_twoopt_pair(TwoOptArgs t, cudaStream_t s) {
+  if (t.n <= 128 || t.n > 256 || t.passes != 1) return QSB_EUNSUPPORTED;
+  TwoOptPair g{};
+  g.kb = (t.n + 31) / 32 * 32;
+  const size_t smem = TwoOptPair::smem_bytes(t.n, g.kb);
+  static size_t attr_dev[MAX_DEV] = {};
+  size_t& attr = attr_dev[cur_dev()];
+  if (smem > attr) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, twoopt_pair_kernel);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (smem + fa.sharedSizeBytes > smem_optin()) return QSB_EUNSUPPORTED;
+    e = cudaFuncSetAttribute(twoopt_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr = smem;
+  }
+  const int64_t cap = num_sms() / 2;
+  const int64_t pairs = t.P < cap ? t.P : cap;
+  if (pairs <= 0) return QSB_OK;
+  twoopt_pair_kernel<<<(int)(2 * pairs), TP2_NT, smem, s>>>(t, g);
+  return launch_status();
+}
+
 // n <= 32: four particles per CTA share one MMA batch (twoopt_tc4_kernel)
 static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
   constexpr int NT = 128;
@@ -334,13 +360,16 @@ static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
   return launch_status();
 }
 
-// QSB_TWOOPT_KERNEL=dp4a | tc (A/B knobs): the dp4a kernel, or the
-// unpipelined tensor-core kernel for every n
+// QSB_TWOOPT_KERNEL=dp4a | tc | pair (A/B knobs): the dp4a kernel, the
+// unpipelined tensor-core kernel for every n, or the CTA-pair kernel
+// (twoopt_pair.cuh; correct, slower than the one-SM pipeline so far)
+// instead of twoopt_tcp_kernel at 128 < n <= 256
 static int twoopt_knob() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("QSB_TWOOPT_KERNEL");
-    v = (e && strcmp(e, "dp4a") == 0) ? 1 : (e && strcmp(e, "tc") == 0) ? 2 : 0;
+    v = (e && strcmp(e, "dp4a") == 0) ? 1 : (e && strcmp(e, "tc") == 0) ? 2
+      : (e && strcmp(e, "pair") == 0) ? 3 : 0;
   }
   return v;
 }
@@ -351,7 +380,9 @@ static int dispatch_twoopt(const TwoOptArgs& t, cudaStream_t s, bool bytes = fal
   if constexpr (sizeof(MT) == 2) {
     if (bytes && t.sym && t.n <= 256 && !twoopt_use_dp4a()) {
       int rc = QSB_EUNSUPPORTED;
-      if (t.n > 128 && t.passes == 1 && twoopt_knob() == 0) rc = launch_twoopt_tcp(t, s);
+      if (t.n > 128 && t.passes == 1 && twoopt_knob() == 3) rc = launch_twoopt_pair(t, s);
+      if (rc == QSB_EUNSUPPORTED && t.n > 128 && t.passes == 1 && (twoopt_knob() == 0 || twoopt_knob() == 3))
+        rc = launch_twoopt_tcp(t, s);
       if (rc == QSB_EUNSUPPORTED)
         rc = t.n <= 32 ? launch_twoopt_tc4(t, s)
            : t.n <= 128 ? launch_twoopt_tc<128>(t, s) : launch_twoopt_tc<256>(t, s);
@@ -374,6 +405,9 @@ int qsb_version(void) { return 10000; }
 #ifdef QSB_TCP_TIMING
 int qsb_debug_tcp_stamps(long long* out) {   // 64 x 10 clock64 stamps (diagnosis build only)
   return cuda_status(cudaMemcpyFromSymbol(out, qsb_tcp_ts, sizeof(long long) * 640));
+}
+int qsb_debug_pair_stamps(long long* out) {  // 64 x 12 clock64 stamps (diagnosis build only)
+  return cuda_status(cudaMemcpyFromSymbol(out, qsb_pair_ts, sizeof(long long) * 768));
 }
 #endif
 

@@ -719,7 +719,7 @@ __device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) 
     asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
                  "selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000u) : "memory");
     if (ok) return;
-    __nanosleep(64);      // a parked warp issues nothing (try_wait alone returned after ~100 cycles)
+    __nanosleep(128);     // a parked warp issues nothing (try_wait alone returned after ~100 cycles)
     if (spins > (1u << 24)) __trap();
   }
 }
@@ -1039,12 +1039,14 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
       const int64_t cost0 = a.cost[p];
       const int64_t pl0 = a.do_pbest ? a.pl_cost[p] : 0;
       asm volatile("bar.sync 1, %0;" :: "r"(32 * TCP_EPI) : "memory");
-      best = redd[TCP_EPI * b];
-      bq = redq[TCP_EPI * b];
-#pragma unroll 1
-      for (int w = 1; w < TCP_EPI; ++w) {
-        const int64_t ob = redd[TCP_EPI * b + w];
-        const int oq = redq[TCP_EPI * b + w];
+      // the epilogue warps' minima: lane l < TCP_EPI takes warp l's, then a
+      // shuffle reduction (every warp computes the same result)
+      best = lane < TCP_EPI ? redd[TCP_EPI * b + lane] : INT64_MAX;
+      bq = lane < TCP_EPI ? redq[TCP_EPI * b + lane] : INT_MAX;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t ob = __shfl_xor_sync(FULL, best, o);
+        const int oq = __shfl_xor_sync(FULL, bq, o);
         if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
       }
       const bool move = bq != INT_MAX && best < 0;

@@ -562,3 +562,30 @@ def test_run_without_stats_uses_graphs_and_matches(golden_instances):
     assert (r1.best_cost, r1.best_iteration, r1.iterations_run) == (st.best_cost, st.best_iteration, 40)
     assert r1.best_perm.tolist() == st.best_perm.tolist()
     assert [tuple(e) for e in r1.migration_events] == [tuple(e) for e in st.migration_log]
+
+
+def test_twoopt_pair_kernel_vs_oracle():
+    """The CTA-pair 2-opt (twoopt_pair.cuh, tcgen05.mma.cta_group::2, opt-in
+    QSB_TWOOPT_KERNEL=pair) equals the oracle on 400 particles at n = 200 and
+    256; run in a subprocess because the knob is read once per process."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1504_05158_b200 import batch; from oracle import oracle as orc\n"
+        "for n in (200, 256):\n"
+        "    rng = np.random.default_rng(n)\n"
+        "    f = np.triu(rng.integers(0, 256, (n, n)), 1); d = np.triu(rng.integers(0, 256, (n, n)), 1)\n"
+        "    f, d = np.minimum(f + f.T, 255), np.minimum(d + d.T, 255)\n"
+        "    perms = np.array([rng.permutation(n) for _ in range(400)], dtype=np.int64)\n"
+        "    c = np.zeros(400, np.int64); orc.cost_many(perms, f, d, c)\n"
+        "    a_p, a_c, b_p, b_c = perms.copy(), c.copy(), perms.copy(), c.copy()\n"
+        "    orc.twoopt_many(a_p, f, d, a_c, 1); batch.twoopt_many(b_p, f, d, b_c, 1)\n"
+        "    assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c), n\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, QSB_TWOOPT_KERNEL="pair")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
