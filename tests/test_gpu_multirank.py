@@ -206,3 +206,36 @@ def test_ring_final_best_distribution_matches_rank_migration():
                                  collect_stats=False).best_cost for s in seeds])
     p = mannwhitneyu(ring_best, ref_best, alternative="two-sided").pvalue
     assert p > 0.01, (p, np.median(ring_best), np.median(ref_best))
+
+
+def test_nccl_exchange_captured_in_graph_equals_eager():
+    """The NCCL path of the sharded exchange, captured in step_many's CUDA
+    graph: a one-rank NCCL process group (the only NCCL world one GPU
+    allows) runs shard.make_exchange -- mode-1 plan/pack, an NCCL all-reduce
+    of the donor records, mode-2 apply -- inside the captured graph, and the
+    trajectory equals eager single-device steps bit for bit."""
+    import paper_1504_05158_b200 as qsb
+    from paper_1504_05158_b200 import shard
+    if not dist.is_nccl_available():
+        pytest.skip("NCCL backend not built")
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        inst = qsb.taillard_uniform(20)
+        cfg = qsb.SolverConfig(swarms=6, swarm_size=12, seed=17, precision="fp32",
+                               migration_factor=0.34, migration_period=2,
+                               coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+        ref = qsb.init_population(cfg, inst)
+        for _ in range(13):
+            qsb.step(ref, inst, cfg)
+        st = qsb.init_population(cfg, inst)
+        qsb.step_many(st, inst, cfg, 13, exchange=shard.make_exchange(1))
+        torch.cuda.synchronize()
+        assert np.array_equal(st.perms, ref.perms)
+        assert np.array_equal(st.bests.costs, ref.bests.costs)
+        assert np.array_equal(st.bests.perms, ref.bests.perms)
+        assert st.V.tobytes() == ref.V.tobytes()
+    finally:
+        dist.destroy_process_group()
