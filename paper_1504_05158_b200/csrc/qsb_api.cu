@@ -96,7 +96,7 @@ static int mw_defer() {
 }
 
 // ------------------------------------------------------------ fused step
-template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false>
 static int launch_step(const StepArgs& a, cudaStream_t s) {
   using K = StepKernel<VT, MT, G, CPL, W, GT>;
   StepArgs b = a;
@@ -108,7 +108,7 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   b.fd_smem = need_fd && (G == 1 || (!a.cost_incremental && K::smem_bytes(a.n, a.vstride, true) <= smem_optin()));
   const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
-  auto fn = step_kernel<VT, MT, G, CPL, W, GT>;
+  auto fn = step_kernel<VT, MT, G, CPL, W, GT, FAST>;
   static size_t attr_smem[MAX_DEV] = {};
   static size_t occ_smem[MAX_DEV] = {};
   static int occ_blocks[MAX_DEV] = {};
@@ -142,6 +142,10 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
         if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin())
           return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16>(a, s);
       } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
+        // the headline case gets the compile-time specialised kernel
+        const bool fast = a.vcol && a.coef && !a.inj_draws && (a.n % 2) == 0 &&
+                          a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V);
+        if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true>(a, s);
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16>(a, s);
       } else if (StepKernel<VT, MT, 1, 2, 8>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 8>(a, s);

@@ -1077,7 +1077,12 @@ __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t 
 }
 
 // ------------------------------------------------------------------------
-template <typename VT, typename MT, int G, int CPL, int W, bool GT = false>
+// FAST: the throughput step of a lazily scaled fp32 state with every phase,
+// the draw pre-pass, no injected draws and even n (engine.step's common
+// case).  Those runtime switches become compile-time constants, so the
+// paths of the other modes drop out of the kernel body and the hot code
+// packs into fewer instruction-cache lines.
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false>
 // Minimum resident CTAs: one-warp kernels QSB_MINB * 4 warps per SM; the
 // multi-warp groups two 8-warp fp32 CTAs with the tile in global memory (n = 256;
 // fp64 would spill, smem tiles allow one CTA anyway) or five
@@ -1100,13 +1105,13 @@ step_kernel(const __grid_constant__ StepArgs a) {
   // (multi-warp groups too, since round 2: the global-memory tile (GT)
   // included; each thread owns one column and rescans its own column)
   constexpr bool kLazy = sizeof(VT) == 4 && (G > 1 || !GT);
-  const bool lazy = kLazy && a.vcol != nullptr && (G == 1 || !a.mw_defer);
+  const bool lazy = FAST || (kLazy && a.vcol != nullptr && (G == 1 || !a.mw_defer));
   const bool wide = lazy;   // lazily scaled fp32 tiles hold wide words (vval)
   // multi-warp fp32 kernels with a column-scale array: deferred column
   // normalisation -- the tile keeps the unnormalised velocity u and row 0
   // of vcol the column scale s (v = u * s), so a step reads and writes every
   // entry once, with no second (rescale) pass over the tile
-  const bool defer = sizeof(VT) == 4 && G > 1 && a.vcol != nullptr && !lazy;
+  const bool defer = !FAST && sizeof(VT) == 4 && G > 1 && a.vcol != nullptr && !lazy;
 
   // PDL: everything below may read what the previous kernel (coef_kernel,
   // best_kernel, migrate_kernel, 2-opt) wrote
@@ -1114,7 +1119,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
   const int nn = n * n;
-  const bool fds = a.fd_smem;
+  const bool fds = FAST || a.fd_smem;
   MT* sF = reinterpret_cast<MT*>(smem);
   MT* sD = sF + nn;
   const int gidx = threadIdx.x / NT;
@@ -1129,11 +1134,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
   int64_t* s_cost = reinterpret_cast<int64_t*>(stg + K::SCOST);
   Scratch& sc = *reinterpret_cast<Scratch*>(stg + K::stage_bytes());
 
-  const bool do_vel = a.flags & F_VELOCITY;
-  const bool do_agg = a.flags & F_AGGREGATE;
-  const bool do_cost = a.flags & F_COST;
-  const bool do_pbest = a.flags & F_PBEST;
-  const bool store_v = a.flags & F_STORE_V;
+  const bool do_vel = FAST || (a.flags & F_VELOCITY);
+  const bool do_agg = FAST || (a.flags & F_AGGREGATE);
+  const bool do_cost = FAST || (a.flags & F_COST);
+  const bool do_pbest = FAST || (a.flags & F_PBEST);
+  const bool store_v = FAST || (a.flags & F_STORE_V);
 
   const MT* cF = sF;
   const MT* cD = sD;
@@ -1200,7 +1205,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   const int vcs = a.vcstride;
   const uint32_t col_bytes = (uint32_t)(5 * vcs * sizeof(float));
   // staged perm rows need 4-byte aligned rows (n even)
-  const bool stage_perm = K::STAGE && (n % 2) == 0;
+  const bool stage_perm = K::STAGE && (FAST || (n % 2) == 0);
   const bool stage_cost = K::STAGE && do_cost && a.cost_incremental && !kFloatMat;
   const bool stage_pl = K::STAGE && do_pbest && do_cost;
   int cbuf = 0;   // s_cost buffer of the particle being processed
@@ -1247,7 +1252,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // no registers across the particle
     auto mkdr = [&]() -> DrawKey {
       DrawKey d;
-      d.inj = a.inj_draws ? a.inj_draws + p * a.inj_stride : nullptr;
+      d.inj = (!FAST && a.inj_draws) ? a.inj_draws + p * a.inj_stride : nullptr;
       d.seed = a.seed;
       d.word1 = word1;
       d.base = (uint64_t)(a.p0 + p) * (uint64_t)row_w;
@@ -1304,7 +1309,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
     }
     double c2r2 = 0.0, c3r3 = 0.0;
     if (do_vel) {
-      if (a.coef) {
+      if (FAST || a.coef) {
         const double* cf = K::STAGE ? s_coef : a.coef + 2 * p;
         c2r2 = cf[0]; c3r3 = cf[1];
       } else {
