@@ -144,7 +144,9 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
       } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
         // the headline case gets the compile-time specialised kernel
         const bool fast = a.vcol && a.coef && !a.inj_draws && (a.n % 2) == 0 &&
-                          a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V);
+                          a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V) &&
+                          a.mode == MODE_SECOND_TARGET && a.depth > 0 && a.normalize && a.v_bounded &&
+                          a.cost_incremental && a.acc32 && a.symmetric && sizeof(MT) <= 2;
         if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true>(a, s);
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16>(a, s);
       } else if (StepKernel<VT, MT, 1, 2, 8>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {

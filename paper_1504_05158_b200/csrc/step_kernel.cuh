@@ -1139,6 +1139,15 @@ step_kernel(const __grid_constant__ StepArgs a) {
   const bool do_cost = FAST || (a.flags & F_COST);
   const bool do_pbest = FAST || (a.flags & F_PBEST);
   const bool store_v = FAST || (a.flags & F_STORE_V);
+  // FAST also fixes the steady-state properties of that case: norm S_v,
+  // second-target S_x with depth > 0, |c1 v| <= v_max, symmetric integral
+  // instance with 32-bit goal sums, cost[p] current
+  const bool normalize = FAST || a.normalize;
+  const bool v_bounded = FAST || a.v_bounded;
+  const bool cost_incr = FAST || a.cost_incremental;
+  const bool acc32 = FAST || a.acc32;
+  const bool symmetric = FAST || a.symmetric;
+  const int mode = FAST ? (int)MODE_SECOND_TARGET : a.mode;
 
   const MT* cF = sF;
   const MT* cD = sD;
@@ -1206,7 +1215,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   const uint32_t col_bytes = (uint32_t)(5 * vcs * sizeof(float));
   // staged perm rows need 4-byte aligned rows (n even)
   const bool stage_perm = K::STAGE && (FAST || (n % 2) == 0);
-  const bool stage_cost = K::STAGE && do_cost && a.cost_incremental && !kFloatMat;
+  const bool stage_cost = K::STAGE && do_cost && cost_incr && !kFloatMat;
   const bool stage_pl = K::STAGE && do_pbest && do_cost;
   int cbuf = 0;   // s_cost buffer of the particle being processed
   // p / S via a reciprocal: p < 2^24 (host limit), so p * (1/S) is within
@@ -1325,11 +1334,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
     // renormalises: u := v, s := 1 / sum |v|)
     bool incr = false;
     if (lazy && do_vel) {
-      bool ok = a.v_bounded && a.c1 > 0.0;
+      bool ok = v_bounded && a.c1 > 0.0;
       const float c1f = (float)a.c1;
       // |lin| of a touched entry is at most lb (the clamp, and c1 + c2 + c3
       // for normalised columns), so u' = lin / (c1 s) stays below 2^125
-      const float lb = fminf((float)a.vmax, a.normalize ? (float)(a.c1 + a.c2 + a.c3) : INFINITY);
+      const float lb = fminf((float)a.vmax, normalize ? (float)(a.c1 + a.c2 + a.c3) : INFINITY);
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
@@ -1397,7 +1406,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
             } else {
               lin = __dadd_rn(__dadd_rn(__dmul_rn(a.c1, v), z2), z3);
             }
-            if (!a.v_bounded || special) {
+            if (!v_bounded || special) {
               if (lin > a.vmax) lin = a.vmax;
               else if (lin < -a.vmax) lin = -a.vmax;
             }
@@ -1478,7 +1487,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           vi.cfree[k] = cfree[k]; vi.cs[k] = cs[k]; vi.csd[k] = csd[k];
         }
         const VelOut<CPL> vo = vel_full_f32<G, CPL>(reinterpret_cast<float*>(tile), n, vi, a.c1, c2r2,
-                                                    c3r3, a.vmax, a.v_bounded, wide, GT && defer && do_agg);
+                                                    c3r3, a.vmax, v_bounded, wide, GT && defer && do_agg);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) total[k] = (VT)vo.total[k];
         if (GT && defer && do_agg) {
@@ -1503,7 +1512,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       nmax[k] = (VT)(-INFINITY); ncnt[k] = 0; nrow[k] = -1; nk64[k] = 0; zkey[k] = 0; zel[k] = false;
-      scale[k] = !lazy && !defer && cfree[k] && do_vel && a.normalize && total[k] > (VT)0;
+      scale[k] = !lazy && !defer && cfree[k] && do_vel && normalize && total[k] > (VT)0;
       inv[k] = (VT)1;
       if constexpr (sizeof(VT) == 4) inv[k] = scale[k] ? 1.0f / total[k] : 1.0f;
     }
@@ -1641,7 +1650,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
           // the new scale as a wide word (double range, so no renormalising pass)
-          sK[k] = wenc((a.normalize && cA[k] > 0.0) ? drcp_approx(cA[k]) : (incr ? c1sdk[k] : 1.0));
+          sK[k] = wenc((normalize && cA[k] > 0.0) ? drcp_approx(cA[k]) : (incr ? c1sdk[k] : 1.0));
         stats_done = true;
       }
     }
@@ -1700,7 +1709,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (!cfree[k]) continue;
-        sK[k] = !do_vel ? cs[k] : ((a.normalize && total[k] > (VT)0) ? 1.0f / (float)total[k] : 1.0f);
+        sK[k] = !do_vel ? cs[k] : ((normalize && total[k] > (VT)0) ? 1.0f / (float)total[k] : 1.0f);
         sc.sS[col[k]] = sK[k];
         if (do_vel && store_v) vs[col[k]] = sK[k];
       }
@@ -1744,10 +1753,10 @@ step_kernel(const __grid_constant__ StepArgs a) {
       }
       int cursor = a.agg_base;     // next aggregation draw (column in the draw row)
 
-      if (a.mode == MODE_PICK_COLUMN) {
+      if (mode == MODE_PICK_COLUMN) {
         agg_pick_column<VT, G, NW>(tile, n, sc, rf, mkdr(), cursor, tid, lane);
       } else {
-        bool restricted = (a.mode == MODE_SECOND_TARGET) && a.depth > 0;
+        bool restricted = (mode == MODE_SECOND_TARGET) && a.depth > 0;
         // cached per-column candidate: (key, tie count, first row) of the
         // column's best eligible cell; recomputed only when its parts change
         uint64_t ck[CPL];
@@ -2212,7 +2221,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       //                + sum_{i not in C, j in C} F[i][j] (D'[i][j] - D[i][j])
       // with D[i][j] = D[p_i][p_j].  Exact in int64 (mod 2^64, as the full
       // sum).  Needs cost[p] == goal(perm[p]) on entry (host guarantee).
-      if (do_cost && a.cost_incremental && sizeof(MT) <= 2 && a.acc32 && n >= 8) {
+      if (do_cost && cost_incr && sizeof(MT) <= 2 && acc32 && n >= 8) {
         Sync::sync();
         const int c0 = lane, c1 = lane + 32;
         const bool m0 = c0 < n && sc.sperm[c0] != sc.szr[c0];
@@ -2230,7 +2239,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           const int ro0 = c0 < n ? sc.szr[c0] : 0, ro1 = c1 < n ? sc.szr[c1] : 0;
           int wsym[CPL];
 #pragma unroll
-          for (int kk = 0; kk < CPL; ++kk) wsym[kk] = (a.symmetric && !(kk == 0 ? m0 : m1)) ? 2 : 1;
+          for (int kk = 0; kk < CPL; ++kk) wsym[kk] = (symmetric && !(kk == 0 ? m0 : m1)) ? 2 : 1;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             unsigned b = ch[h];
@@ -2249,7 +2258,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 if (col[kk] < n)
                   part += wsym[kk] * (int)cF[i * n + col[kk]] *
                           ((int)cD[pin * n + pjn[kk]] - (int)cD[pio * n + pjo[kk]]);
-              if (!a.symmetric) {
+              if (!symmetric) {
                 if (c0 < n && !m0) part += (int)cF[c0 * n + i] * ((int)cD[ro0 * n + pin] - (int)cD[ro0 * n + pio]);
                 if (c1 < n && !m1) part += (int)cF[c1 * n + i] * ((int)cD[ro1 * n + pin] - (int)cD[ro1 * n + pio]);
               }
@@ -2273,7 +2282,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       // terms of its own columns j over i in C (integer sums: the list order
       // does not matter).  At n = 256 |C| is a few, against the n^2 terms of
       // the full goal.
-      if (do_cost && a.cost_incremental && sizeof(MT) <= 2 && a.acc32 && n >= 8) {
+      if (do_cost && cost_incr && sizeof(MT) <= 2 && acc32 && n >= 8) {
         bool mv[CPL];
         if (tid == 0) sc.ssel[2] = 0;
         Sync::sync();
@@ -2293,14 +2302,14 @@ step_kernel(const __grid_constant__ StepArgs a) {
             const int pjn = sc.sperm[j], pjo = sc.szr[j];
             // symmetric F, D: an unmoved column's term for row i in C equals
             // its row's term for column i, which then counts twice
-            const int w = (a.symmetric && !mv[k]) ? 2 : 1;
+            const int w = (symmetric && !mv[k]) ? 2 : 1;
 #pragma unroll 4
             for (int c = 0; c < kc; ++c) {
               const int i = sc.srow[c];
               const int pin = sc.sperm[i], pio = sc.szr[i];
               // n max(F) max(D) < 2^32 and n >= 8: each term fits int32
               acc += (int64_t)(w * (int)cF[i * n + j] * ((int)cD[pin * n + pjn] - (int)cD[pio * n + pjo]));
-              if (!a.symmetric && !mv[k])
+              if (!symmetric && !mv[k])
                 acc += (int64_t)((int)cF[j * n + i] * ((int)cD[pjo * n + pin] - (int)cD[pjo * n + pio]));
             }
           }
@@ -2318,7 +2327,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       }
     }
     if (do_cost && !cost_done) {
-      const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane, a.acc32);
+      const int64_t tot = cost_general<MT, G, CPL>(cF, cD, n, sc, tid, lane, acc32);
       if (tid == 0) reinterpret_cast<int64_t*>(a.cost)[p] = tot;   // raw bits for doubles
       ncost = tot;
       cost_done = true;
