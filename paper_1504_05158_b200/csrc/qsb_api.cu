@@ -132,22 +132,34 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   return launch_pdl(fn, grid, 32 * G * W, smem, s, b);
 }
 
+// The steady-state throughput case (lazily scaled fp32 state, every phase,
+// draw pre-pass, no injected draws, norm S_v, second-target S_x, bounded
+// velocity, symmetric integral instance with 32-bit goal sums, current
+// costs, even n) runs compile-time specialised kernels (step_kernel FAST).
+static bool fast_case(const StepArgs& a, size_t mt_size) {
+  return a.vcol && !a.mw_defer && a.coef && !a.inj_draws && (a.n % 2) == 0 &&
+         a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V) &&
+         a.mode == MODE_SECOND_TARGET && a.depth > 0 && a.normalize && a.v_bounded &&
+         a.cost_incremental && a.acc32 && a.symmetric && mt_size <= 2;
+}
+
 template <typename VT, typename MT, bool DRY>
 static int dispatch_n(const StepArgs& a, cudaStream_t s) {
+  constexpr bool kFastType = sizeof(VT) == 4 && sizeof(MT) == 2;
+  const bool fast = kFastType && fast_case(a, sizeof(MT));
   // one-warp groups: fp32 tiles run 16 particles per CTA where they fit (one
   // CTA per SM, F / D staged once per SM), else 8; fp64 tiles 4 per CTA
   if (a.n <= 64) {
     if constexpr (sizeof(VT) == 4) {
       if (a.n <= 32) {
-        if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin())
+        if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
+          if constexpr (kFastType)
+            if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16, false, true>(a, s);
           return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16>(a, s);
+        }
       } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
-        // the headline case gets the compile-time specialised kernel
-        const bool fast = a.vcol && a.coef && !a.inj_draws && (a.n % 2) == 0 &&
-                          a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V) &&
-                          a.mode == MODE_SECOND_TARGET && a.depth > 0 && a.normalize && a.v_bounded &&
-                          a.cost_incremental && a.acc32 && a.symmetric && sizeof(MT) <= 2;
-        if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true>(a, s);
+        if constexpr (kFastType)
+          if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true>(a, s);
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16>(a, s);
       } else if (StepKernel<VT, MT, 1, 2, 8>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 8>(a, s);
@@ -162,12 +174,21 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
   }
   if (a.n <= 128) {
     if constexpr (DRY) return StepKernel<VT, MT, 4, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
-    else return launch_step<VT, MT, 4, 1, 1>(a, s);
+    else {
+      if constexpr (kFastType)
+        if (fast) return launch_step<VT, MT, 4, 1, 1, false, true>(a, s);
+      return launch_step<VT, MT, 4, 1, 1>(a, s);
+    }
   }
   if (a.n <= 256) {
     const bool fits = StepKernel<VT, MT, 8, 1, 1>::smem_bytes(a.n, a.vstride, false) <= smem_optin();
     if constexpr (DRY) return QSB_OK;
-    else return fits ? launch_step<VT, MT, 8, 1, 1>(a, s) : launch_step<VT, MT, 8, 1, 1, true>(a, s);
+    else {
+      if constexpr (kFastType)
+        if (fast) return fits ? launch_step<VT, MT, 8, 1, 1, false, true>(a, s)
+                              : launch_step<VT, MT, 8, 1, 1, true, true>(a, s);
+      return fits ? launch_step<VT, MT, 8, 1, 1>(a, s) : launch_step<VT, MT, 8, 1, 1, true>(a, s);
+    }
   }
   return QSB_EUNSUPPORTED;
 }

@@ -1119,7 +1119,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
   const int nn = n * n;
-  const bool fds = FAST || a.fd_smem;
+  const bool fds = (FAST && G == 1) || a.fd_smem;   // multi-warp: F / D via L1 when incremental
   MT* sF = reinterpret_cast<MT*>(smem);
   MT* sD = sF + nn;
   const int gidx = threadIdx.x / NT;
