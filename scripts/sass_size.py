@@ -4,7 +4,7 @@ helpers called from it) and the out-of-line callees.  Usage:
 sass_size.py [mangled-name-substring]"""
 import re, subprocess, sys, collections, tempfile, os
 name = sys.argv[1] if len(sys.argv) > 1 else "step_kernelIftLi1ELi2ELi16ELb0E"
-lib = "paper_1504_05158_b200/libqsb.so"
+lib = sys.argv[2] if len(sys.argv) > 2 else "paper_1504_05158_b200/libqsb.so"
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
 cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
