@@ -1151,25 +1151,6 @@ step_kernel(const __grid_constant__ StepArgs a) {
 
   const MT* cF = sF;
   const MT* cD = sD;
-  if (do_cost) {
-    const MT* gF = reinterpret_cast<const MT*>(a.F);
-    const MT* gD = reinterpret_cast<const MT*>(a.D);
-    if (G == 1 || fds) {
-      if ((nn * sizeof(MT)) % 16 == 0) {
-        // 16-byte copies (sD = sF + nn stays aligned)
-        const int nv = (int)(nn * sizeof(MT) / 16);
-        const uint4* gF4 = reinterpret_cast<const uint4*>(gF);
-        const uint4* gD4 = reinterpret_cast<const uint4*>(gD);
-        uint4* sF4 = reinterpret_cast<uint4*>(sF);
-        uint4* sD4 = reinterpret_cast<uint4*>(sD);
-        for (int i = threadIdx.x; i < nv; i += blockDim.x) { sF4[i] = gF4[i]; sD4[i] = gD4[i]; }
-      } else {
-        for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
-      }
-    } else {
-      cF = gF; cD = gD;
-    }
-  }
   if (tid == 0) { mbar_init(&sc.bar, 1); mbar_fence_init(); }
   for (int c = tid; c < K::NMAX; c += NT) { sc.stie[c] = 0; sc.sS[c] = 1.0f; }
   if (tid == 0) sc.wide = wide;
@@ -1231,6 +1212,29 @@ step_kernel(const __grid_constant__ StepArgs a) {
     issue_particle_load<K, VT>(&a, pp, buf, tid, lane, tile, stg, &sc.bar, tile_bytes, col_bytes, lflags,
                                inv_s);
   };
+  // the first particle's operands are requested before F and D are staged,
+  // so the two loads overlap (each warp's first tile is not prefetched)
+  if (!GT && p < a.P) { issue_load(p, cbuf); loaded = true; }
+  if (do_cost) {
+    const MT* gF = reinterpret_cast<const MT*>(a.F);
+    const MT* gD = reinterpret_cast<const MT*>(a.D);
+    if (G == 1 || fds) {
+      if ((nn * sizeof(MT)) % 16 == 0) {
+        // 16-byte copies (sD = sF + nn stays aligned)
+        const int nv = (int)(nn * sizeof(MT) / 16);
+        const uint4* gF4 = reinterpret_cast<const uint4*>(gF);
+        const uint4* gD4 = reinterpret_cast<const uint4*>(gD);
+        uint4* sF4 = reinterpret_cast<uint4*>(sF);
+        uint4* sD4 = reinterpret_cast<uint4*>(sD);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) { sF4[i] = gF4[i]; sD4[i] = gD4[i]; }
+      } else {
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) { sF[i] = gF[i]; sD[i] = gD[i]; }
+      }
+    } else {
+      cF = gF; cD = gD;
+    }
+  }
+  __syncthreads();
   while (p < a.P) {
     const unsigned q_next = a.work ? claim() : 0u;
     int64_t p_next = -1;
