@@ -373,6 +373,7 @@ def main():
         else:
             from paper_1504_05158_b200 import _lib
             rt = engine._runtime(state, inst, cfg)
+            rt.coeffs.hints &= ~_lib.HINT_COEF_READY   # this leg draws its own coefficients
             s = state.stream()
             timer.before(s)
             _lib.call("qsb_step_phases", state.c_state(), rt.inst, rt.coeffs, flags, None, 0, 2,
@@ -537,7 +538,9 @@ def main():
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": traffic_from_profile(args.n, cfg.precision, state.local_particles,
                                                 "velocity_only_" if flags is not None else ""),
-                "kernel": "coef_kernel + step_kernel (draw pre-pass; fused velocity+aggregation+goal+pbest)" if flags is None
+                "kernel": ("step_kernel (fused velocity+aggregation+goal+pbest; draws made by the previous best_kernel)"
+                           if engine._COEF_FOLD else
+                           "coef_kernel + step_kernel (draw pre-pass; fused velocity+aggregation+goal+pbest)") if flags is None
                           else "step_kernel velocity-only build",
                 "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
                 "algorithmic_bytes_per_particle": "SURVEY §8(d) B_vel = 2 n^2 s_V + 4 n + 2 n / S"

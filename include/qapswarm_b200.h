@@ -143,6 +143,10 @@ typedef struct qsb_coeffs {
 /* flow and distance are symmetric (integral instances): the incremental goal
  * counts the unmoved rows' column terms through the moved rows' row terms. */
 #define QSB_HINT_SYMMETRIC 4
+/* st->step_coef already holds this step's (c2 r2, c3 r3) and st->work is
+ * zero: the previous step ended with qsb_best_update_next (same seed, c2,
+ * c3), so qsb_step_phases launches no pre-pass. */
+#define QSB_HINT_COEF_READY 8
 
 /* One migration event (migration.migrate, migration.py:55-86). */
 typedef struct qsb_migration {
@@ -191,6 +195,12 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
 /* Swarm bests (argmin over improved particles, strict <) and the global best
  * (argmin over all, strict <), engine.py:216-229; advances *iteration. */
 int qsb_best_update(const qsb_state* st, void* stream);
+
+/* qsb_best_update plus the NEXT step's draw pre-pass: (c2 r2, c3 r3) of
+ * iteration t + 1 for every particle into st->step_coef, and st->work reset
+ * (the pre-pass of qsb_step_phases, folded into the best-update launch).
+ * Follow it with qsb_step_phases under QSB_HINT_COEF_READY. */
+int qsb_best_update_next(const qsb_state* st, const qsb_coeffs* co, void* stream);
 
 /* One full iteration: qsb_step_phases(all) + qsb_best_update.  The caller
  * swaps perm/perm_new afterwards (engine.py:231-232). */

@@ -22,6 +22,7 @@ PHASE_VELOCITY, PHASE_AGGREGATE, PHASE_COST, PHASE_PBEST, PHASE_STORE_V = 1, 2, 
 HINT_V_BOUNDED = 1
 HINT_COST_CURRENT = 2
 HINT_SYMMETRIC = 4
+HINT_COEF_READY = 8
 TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
 TWOOPT_BYTES = 4
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V
@@ -89,6 +90,7 @@ SIGNATURES = {
                                        ctypes.POINTER(QsbCoeffs), _i32, _vp, _i64, _i32, _vp,
                                        _u64, _vp]),
     "qsb_best_update": (ctypes.c_int, [ctypes.POINTER(QsbState), _vp]),
+    "qsb_best_update_next": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbCoeffs), _vp]),
     "qsb_step": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbInstance),
                                 ctypes.POINTER(QsbCoeffs), _vp]),
     "qsb_migrate": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbMigration), _vp]),

@@ -29,6 +29,12 @@ struct BestArgs {
   void* swarm_min;       // (m,) scratch: per-swarm min cost over all particles
   int64_t* swarm_min_idx;
   unsigned* done;        // arrival counter (zero-initialised)
+  // the next step's draw pre-pass (qsb_best_update_next), or coef == null
+  double* coef;          // (P, 2): c2 r2, c3 r3 of iteration t + 1
+  double c2, c3;
+  uint64_t seed;
+  int64_t P;             // local particles
+  unsigned* work;        // the step kernel's particle counter, reset here
 };
 
 template <typename CT>
@@ -63,6 +69,25 @@ __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
   const int64_t k = (int64_t)blockIdx.x * WPB + (threadIdx.x >> 5);
   const CT* cost = reinterpret_cast<const CT*>(a.cost);
   const int n = a.n;
+  if (a.coef) {
+    // the next step's (c2 r2, c3 r3): exactly coef_kernel's stream and
+    // arithmetic for iteration t + 1 (this grid advances *t_dev to t at its
+    // end, so t + 1 = *t_dev + 2 here), and the particle counter reset
+    if (a.work && blockIdx.x == 0 && threadIdx.x == 0) *a.work = 0u;
+    const uint64_t word1 = stream_word(2, (uint64_t)(*a.t_dev) + 2);
+    const uint64_t w = 2 + 2 * (uint64_t)n;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t idx = (uint64_t)(a.p0 + p) * w;
+      const PhiloxBlock b = philox4x64_10((idx >> 2) + 1, a.seed, word1);
+      const unsigned l = (unsigned)(idx & 3);   // w is even: l is 0 or 2
+      double u0, u1;
+      if (l == 0) { u0 = u64_to_unit(b.v[0]); u1 = u64_to_unit(b.v[1]); }
+      else { u0 = u64_to_unit(b.v[2]); u1 = u64_to_unit(b.v[3]); }
+      a.coef[2 * p] = __dmul_rn(a.c2, u0);
+      a.coef[2 * p + 1] = __dmul_rn(a.c3, u1);
+    }
+  }
   if (k < a.m) {
     CT bi = ct_max<CT>(), ba = ct_max<CT>();
     int64_t ii = INT64_MAX, ia = INT64_MAX;

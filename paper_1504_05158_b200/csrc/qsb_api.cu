@@ -518,7 +518,11 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
   a.agg_base = agg_base;
   a.coef = coef;
   bool work_reset = false;
-  if (!coef && !inj_draws && (flags & QSB_PHASE_VELOCITY) && st->step_coef && st->num_particles > 0) {
+  if (!coef && !inj_draws && (flags & QSB_PHASE_VELOCITY) && st->step_coef && (co->hints & QSB_HINT_COEF_READY)) {
+    // the previous step's best update drew this step's coefficients
+    a.coef = st->step_coef;
+    work_reset = true;
+  } else if (!coef && !inj_draws && (flags & QSB_PHASE_VELOCITY) && st->step_coef && st->num_particles > 0) {
     // the step's (c2 r2, c3 r3) from a one-thread-per-particle pre-pass
     const int64_t P = st->num_particles;
     const int grid = (int)((P + 255) / 256 < 4 * num_sms() ? (P + 255) / 256 : 4 * num_sms());
@@ -538,9 +542,26 @@ int qsb_step_phases(const qsb_state* st, const qsb_instance* inst, const qsb_coe
   return dispatch<false>(st->v_dtype, mat, a, (cudaStream_t)stream);
 }
 
-int qsb_best_update(const qsb_state* st, void* stream) {
+static int best_update(const qsb_state* st, const qsb_coeffs* co, void* stream);
+
+int qsb_best_update(const qsb_state* st, void* stream) { return best_update(st, nullptr, stream); }
+
+int qsb_best_update_next(const qsb_state* st, const qsb_coeffs* co, void* stream) {
+  if (!co || !st || !st->step_coef) return QSB_EINVAL;
+  return best_update(st, co, stream);
+}
+
+static int best_update(const qsb_state* st, const qsb_coeffs* co, void* stream) {
   if (!st || !st->iteration || !st->done) return QSB_EINVAL;
   BestArgs b{};
+  if (co) {
+    b.coef = st->step_coef;
+    b.c2 = co->c2;
+    b.c3 = co->c3;
+    b.seed = co->seed;
+    b.P = st->num_particles;
+    b.work = (unsigned*)st->work;
+  }
   b.n = st->n;
   b.S = st->swarm_size;
   b.m = st->num_swarms;

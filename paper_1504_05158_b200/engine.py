@@ -59,6 +59,8 @@ def projected_buffer_bytes(config: SolverConfig, n: int) -> int:
 # column-state rows); the one-warp kernels since round 1, the multi-warp
 # kernels (n <= 256) since round 2.  QSB_MW_DEFER=1 keeps n > 64 on the
 # deferred column scale (A/B; read by libqsb too).
+# QSB_NO_COEF_FOLD=1: a separate draw pre-pass every step (A/B measurements)
+_COEF_FOLD = _os.environ.get("QSB_NO_COEF_FOLD", "") != "1"
 _LAZY_MAX_N = 64 if _os.environ.get("QSB_MW_DEFER", "") == "1" else 256
 
 
@@ -182,6 +184,9 @@ class PopulationState:
         self.launches = 0         # kernels launched by step() (bench accounting)
         self.v_bound = float("inf")   # proven bound on max |V| (enables QSB_HINT_V_BOUNDED)
         self.cost_current = False     # cost[p] == goal(perm[p]) (enables QSB_HINT_COST_CURRENT)
+        # (t, c2, c3, seed): step_coef holds iteration t's draws, drawn by the
+        # previous best update (enables QSB_HINT_COEF_READY)
+        self.coef_ready = None
 
     # ---------------------------------------------------------- C structs
     def c_state(self) -> _lib.QsbState:
@@ -437,7 +442,9 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
     state.d_iteration.fill_(-1)
     cs = state.c_state()
     cs.perm_new = state.d_perm.data_ptr()
-    _lib.call("qsb_best_update", cs, stream)
+    # (the pass also draws iteration 1's coefficients: *t_dev + 2 = 1)
+    _best_update(cs, rt, stream)
+    state.coef_ready = _coef_key(config, 1)
     state.t = 0
     state._host_best = None
     state.v_bound = float(config.init_velocity_amplitude)
@@ -583,6 +590,22 @@ def _hints(state: PopulationState, rt: "_Runtime", coeffs: PsoCoefficients) -> i
     return hints
 
 
+def _coef_key(config: SolverConfig, t: int):
+    if not _COEF_FOLD:
+        return None
+    c = config.coefficients
+    return (t, float(c.c2), float(c.c3), int(config.seed) & (2**64 - 1))
+
+
+def _best_update(cs, rt: "_Runtime", stream) -> None:
+    """Swarm / global best update; it also draws the next iteration's
+    coefficients (qsb_best_update_next), so that step runs no pre-pass."""
+    if _COEF_FOLD:
+        _lib.call("qsb_best_update_next", cs, rt.coeffs, stream)
+    else:
+        _lib.call("qsb_best_update", cs, stream)
+
+
 def _post_step_v_bound(coeffs: PsoCoefficients) -> float:
     """After S_v every entry is clamped to v_max, or normalised to |v| <= 1."""
     return (1.0 + 1e-6) if coeffs.sv_mode == "norm" else coeffs.v_max
@@ -607,7 +630,8 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
     rt = _runtime(state, instance, config)
     stream = state.stream()
     cs = state.c_state()
-    rt.coeffs.hints = _hints(state, rt, coeffs)
+    ready = _COEF_FOLD and state.coef_ready == _coef_key(config, t)
+    rt.coeffs.hints = _hints(state, rt, coeffs) | (_lib.HINT_COEF_READY if ready else 0)
     passes = config.two_opt_passes
     if passes and not state.integral:
         raise ValueError("two_opt_passes requires an integral instance")
@@ -627,8 +651,10 @@ def step(state: PopulationState, instance, config: SolverConfig, exchange=None,
         if tb is not None:
             timer.after_twoopt(stream)
         state.launches += 1
-    _lib.call("qsb_best_update", cs, stream)
-    state.launches += 3      # draw pre-pass + fused step + best update
+    # the best update also draws iteration t + 1's coefficients
+    _best_update(cs, rt, stream)
+    state.coef_ready = _coef_key(config, t + 1)
+    state.launches += 2 if ready else 3      # [draw pre-pass +] fused step + best update
     state.v_bound = _post_step_v_bound(coeffs)
     state.cost_current = True     # cost[p] is now the goal of the new position
     state.swap_positions()
@@ -674,14 +700,17 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
     span = _graph_span(config)
     # eager steps up to an aligned start (the first one also settles the
     # launch hints: velocity bound and current costs)
-    while steps > 0 and (state.t == 0 or state.t % span != 0 or not state.cost_current):
+    while steps > 0 and (state.t == 0 or state.t % span != 0 or not state.cost_current
+                         or state.coef_ready != _coef_key(config, state.t + 1)):
         step(state, instance, config, exchange=exchange)
         steps -= 1
     reps = steps // span
     if reps >= 1:
         rt = _runtime(state, instance, config)
         coeffs = config.coefficients
-        hints = _hints(state, rt, coeffs)     # valid for every later step (post-S_v bound)
+        # valid for every later step (post-S_v bound; each step's best update
+        # draws the next step's coefficients)
+        hints = _hints(state, rt, coeffs) | (_lib.HINT_COEF_READY if _COEF_FOLD else 0)
         rt.coeffs.hints = hints
         d = config.migration_depth if config.migration_factor > 0.0 else 0
         # rt: the runtime object itself (its device instance is captured)
@@ -725,7 +754,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
                                   None, 0, s)
                         if passes:
                             _lib.call("qsb_twoopt", cs, rt.inst, passes, tf, s)
-                        _lib.call("qsb_best_update", cs, s)
+                        _best_update(cs, rt, s)
                         if mig is not None and (i + 1) % config.migration_period == 0:
                             mst = _lib.QsbState.from_buffer_copy(cs)
                             mst.perm = cs.perm_new           # migration reads the post-swap positions
@@ -739,9 +768,10 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
             graph.replay()
         passes = config.two_opt_passes
         epochs = _due_epochs(config, state.t, state.t + reps * span)
-        state.launches += reps * span * (3 + (1 if passes else 0)) \
+        state.launches += reps * span * (2 + (0 if _COEF_FOLD else 1) + (1 if passes else 0)) \
             + epochs * (1 if exchange is None else 2)
         state.t += reps * span
+        state.coef_ready = _coef_key(config, state.t + 1)
         if state._mig is not None and getattr(exchange, "logs_events", True):
             state._mig.pending += epochs
         state.v_bound = _post_step_v_bound(coeffs)
