@@ -317,6 +317,20 @@ static int launch_twoopt_tcp(TwoOptArgs t, cudaStream_t s) {
   g.kb = (t.n + 31) / 32 * 32;
   g.npad = (t.n + 15) / 16 * 16;
   if (t.n <= 128 || t.n > 256 || t.passes != 1) return QSB_EUNSUPPORTED;
+  // polling pauses of the parked roles (A/B knobs QSB_TCP_SLEEP_EPI / _BLD, ns)
+  static int sl[2] = {-1, -1};
+  if (sl[0] < 0) {
+    const char* e0 = getenv("QSB_TCP_SLEEP_EPI");
+    const char* e1 = getenv("QSB_TCP_SLEEP_BLD");
+    sl[0] = e0 ? atoi(e0) : 128;
+    sl[1] = e1 ? atoi(e1) : 128;
+  }
+  g.sleep_epi = (unsigned)sl[0];
+  g.sleep_bld = (unsigned)sl[1];
+  // second MMA half with A from the tensor-memory copy of P (QSB_TCP_TS=0: both from shared memory)
+  static int ts = -1;
+  if (ts < 0) { const char* e = getenv("QSB_TCP_TS"); ts = (e && e[0] == '0') ? 0 : 1; }
+  g.ts = ts;
   const size_t smem = TwoOptTcp::smem_bytes(t.n, g.kb);
   static size_t attr_dev[MAX_DEV] = {};
   size_t& attr = attr_dev[cur_dev()];

@@ -680,9 +680,12 @@ __global__ void __launch_bounds__(NT) twoopt_tc_kernel(const TwoOptArgs a, const
 // Epilogue warps are spread over the four TMEM lane quarters 4 / 3 / 3 / 2
 // because low rows have more s > r.  Bit-identical to twoopt_tc_kernel.
 // Barriers (CTA mbarriers): full[b] (builders -> MMA issuer and epilogue:
-// P, sv[b], sp[b] written), mma_done (MMA + copy commit -> epilogue, and
-// -> builders: P readable again), hfree (epilogue done with H and the P
-// copy -> next MMA), bfree[b] (epilogue done with sv[b], sp[b]).
+// P, sv[b], sp[b] written), mma0 / mma_done (tile-0 / tile-1 MMA + copy
+// commits -> epilogue; mma_done also -> builders: P readable again),
+// hfree0 / hfree (epilogue done with tile 0's / tile 1's H columns and P
+// copy: the next particle's tile-0 MMA overlaps this particle's tile-1
+// scoring and reduction, its tile-1 MMA the tile-0 scoring of the
+// particle before), bfree[b] (epilogue done with sv[b], sp[b]).
 constexpr int TCP_NT = 768;          // 24 warps, 80 registers each
 constexpr int TCP_EPI = 16;          // epilogue warps
 constexpr int TCP_BLD = 8;           // builder warps (warp 15 issues the MMAs)
@@ -694,14 +697,24 @@ __host__ __device__ constexpr int tcp_eq(int q) { return q == 0 ? 5 : q == 3 ? 3
 
 struct TwoOptTcp {
   int kb, npad;
+  unsigned sleep_epi, sleep_bld;   // ns parked between polls (epilogue / builder waits)
+  int ts;                          // 1: second MMA half with A = the P copy in TMEM
   // D row stride in bytes: an odd number of 4-byte words, so 32 consecutive
   // D rows read at one column fall into 32 distinct banks
   static __host__ __device__ int dstride(int n) { return (((n + 3) / 4) | 1) * 4; }
   static __host__ __device__ size_t smem_bytes(int n, int kb) {
     return 2 * (size_t)256 * kb + align_up((size_t)n * dstride(n), 16) + 2 * 256 * 16 + 2 * 256 * 2 +
-           2 * 256 * 2 + 2 * TCP_EPI * 16;
+           2 * 256 * 2 + 2 * TCP_EPI * 16 + 2 * 256 * 4;
   }
 };
+
+// one lane of a converged warp (elect.sync): issues a single-thread
+// tcgen05 instruction while the operands stay warp-uniform
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(e));
+  return e != 0;
+}
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
@@ -711,7 +724,7 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 // waiting warps do not steal issue slots from the working roles), with a
 // deadlock guard: a launch error (trap) instead of a hung GPU after 2^24
 // unsuccessful polls (each followed by a 64 ns sleep)
-__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity, unsigned sleep_ns = 128) {
   const uint32_t a = smem_u32(bar);
 #pragma unroll 1
   for (uint32_t spins = 0;; ++spins) {
@@ -719,7 +732,7 @@ __device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) 
     asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
                  "selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000u) : "memory");
     if (ok) return;
-    __nanosleep(128);     // a parked warp issues nothing (try_wait alone returned after ~100 cycles)
+    __nanosleep(sleep_ns);  // a parked warp issues nothing (try_wait alone returned after ~100 cycles)
     if (spins > (1u << 24)) __trap();
   }
 }
@@ -739,6 +752,56 @@ __device__ long long qsb_tcp_ts[64][10];
 #define TCP_TS(i, k) do { } while (0)
 #endif
 
+// One row tile's MMAs (H += F P^T over K steps, then P F^T) and the P copy
+// into TMEM, issued by one elected lane of a converged warp.  KS K steps of
+// 32 bytes; a K step is +16 in a no-swizzle descriptor's address field.
+// A operand from tensor memory (the P copy, row r at lane r mod 128, 8
+// columns per 32-byte K step), B from shared memory
+__device__ __forceinline__ void umma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n"
+      :: "r"(d_tmem), "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+// Split issue (TS mode): H = F P^T from shared memory plus the P copy first
+// (after which the P buffer is free for the next particle's builders), then
+// H += P F^T with P read back from tensor memory.
+template <int KS>
+__device__ __forceinline__ void tcp_issue_fp(uint32_t dt, uint64_t f0, uint64_t p0, uint32_t idd, uint32_t pcol) {
+  if (elect_one()) {
+#pragma unroll
+    for (int j = 0; j < KS; ++j) umma_i8(dt, f0 + 16 * j, p0 + 16 * j, idd, j > 0 ? 1u : 0u);
+#pragma unroll
+    for (int k = 0; k < KS; ++k) tmem_cp_128x256b(pcol + 8 * k, p0 + 16 * k);
+  }
+  __syncwarp();
+}
+template <int KS>
+__device__ __forceinline__ void tcp_issue_pf(uint32_t dt, uint32_t pcol, uint64_t f0, uint32_t idd) {
+  if (elect_one()) {
+#pragma unroll
+    for (int j = 0; j < KS; ++j) umma_i8_ts(dt, pcol + 8 * j, f0 + 16 * j, idd, 1u);
+  }
+  __syncwarp();
+}
+
+template <int KS>
+__device__ __forceinline__ void tcp_issue_tile(uint32_t dt, uint64_t f0, uint64_t p0, uint32_t idd,
+                                               uint32_t pcol) {
+  if (elect_one()) {
+#pragma unroll
+    for (int j = 0; j < KS; ++j) umma_i8(dt, f0 + 16 * j, p0 + 16 * j, idd, j > 0 ? 1u : 0u);
+#pragma unroll
+    for (int j = 0; j < KS; ++j) umma_i8(dt, p0 + 16 * j, f0 + 16 * j, idd, 1u);
+    // the epilogue's copy of P: 32 bytes (8 columns) of 128 rows per copy
+#pragma unroll
+    for (int k = 0; k < KS; ++k) tmem_cp_128x256b(pcol + 8 * k, p0 + 16 * k);
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs a, const TwoOptTcp g) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   const int n = a.n, kb = g.kb, npad = g.npad;
@@ -752,15 +815,17 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
   int16_t* pinvb = spb + 512;                                 // [2][256] inverse perm (builders)
   int64_t* redd = reinterpret_cast<int64_t*>(pinvb + 512);   // [2][TCP_EPI]
   int* redq = reinterpret_cast<int*>(redd + 2 * TCP_EPI);    // [2][TCP_EPI]
-  __shared__ __align__(8) uint64_t full[2], bfree[2], mma_done, hfree;
+  int* spwb = redq + 2 * TCP_EPI;                             // [2][256] the perm as words (builders)
+  __shared__ __align__(8) uint64_t full[2], bfree[2], mma0, mma_done, hfree0, hfree, pfree;
   __shared__ uint32_t s_tmem;
   __shared__ unsigned s_mx[2];
+  __shared__ unsigned s_arr[2];   // epilogue warps done with particle idx (buffer b)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint16_t* gF = reinterpret_cast<const uint16_t*>(a.F);
   const uint16_t* gD = reinterpret_cast<const uint16_t*>(a.D);
 
   // ---- prologue: zero the operands, F (canonical) and D (row-major) as bytes
-  if (tid < 2) s_mx[tid] = 0;
+  if (tid < 2) { s_mx[tid] = 0; s_arr[tid] = 0; }
   {
     uint4* z = reinterpret_cast<uint4*>(F8);
     const int nz = (int)(2 * mb / 16);
@@ -799,8 +864,9 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
   if (lane == 0) { atomicMax(&s_mx[0], mf); atomicMax(&s_mx[1], md); }
   if (tid == 0) {
     mbar_init(&full[0], TCP_BLD); mbar_init(&full[1], TCP_BLD);
-    mbar_init(&bfree[0], TCP_EPI); mbar_init(&bfree[1], TCP_EPI);
-    mbar_init(&mma_done, 1); mbar_init(&hfree, TCP_EPI);
+    mbar_init(&bfree[0], 1); mbar_init(&bfree[1], 1);
+    mbar_init(&mma0, 1); mbar_init(&mma_done, 1); mbar_init(&pfree, 1);
+    mbar_init(&hfree0, TCP_EPI); mbar_init(&hfree, TCP_EPI);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -830,13 +896,15 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
       int16_t* pinv = pinvb + 256 * b;      // double-buffered: a fast builder thread may
                                             // start the next particle while others still read
       int4* sv = svb + 256 * b;
-      if (idx >= 2) mbar_wait_guard(&bfree[b], ((idx >> 1) - 1) & 1);    // sv[b], sp[b] free
+      int* spw = spwb + 256 * b;
+      if (idx >= 2) mbar_wait_guard(&bfree[b], ((idx >> 1) - 1) & 1, g.sleep_bld);    // sv[b], sp[b] free
       for (int i = bt; i < n; i += TCP_BLD * 32) {
         const int16_t v = a.perm[p * n + i];
         sp[i] = v;
+        spw[i] = v;
         pinv[v] = (int16_t)i;
       }
-      if (idx >= 1) mbar_wait_guard(&mma_done, (idx - 1) & 1);          // P read by MMA + copy
+      if (idx >= 1) mbar_wait_guard(&pfree, (idx - 1) & 1, g.sleep_bld);   // P read by MMA + copy
       asm volatile("bar.sync 2, %0;" :: "r"(TCP_BLD * 32) : "memory");
       if (bt == 0) TCP_TS(idx, 0);
       // P[i] = D[p_i][p] built by SOURCE row: thread d owns D row d, i.e.
@@ -854,10 +922,42 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
           dr[h] = bt + h * TCP_BLD * 32;
           ir[h] = dr[h] < n ? pinv[dr[h]] : 0;
           drow[h] = D8 + (dr[h] < n ? dr[h] : 0) * dn;
-          acc[h] = 0; pii[h] = 0;
+          acc[h] = 0;
+          pii[h] = dr[h] < n ? drow[h][dr[h]] : 0u;   // P_ii = D[p_i][p_i], p_i = d
         }
+        // full chunks: the 16 column indices as words (four broadcast
+        // loads), one add and one byte load per entry, no bounds tests
+        const int nfull = n >> 4;
 #pragma unroll 1
-        for (int c = 0; c < nck; ++c) {
+        for (int c = 0; c < nfull; ++c) {
+          const int4* q4 = reinterpret_cast<const int4*>(spw + 16 * c);
+          int pj[16];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int4 qq = q4[x];
+            pj[4 * x] = qq.x; pj[4 * x + 1] = qq.y; pj[4 * x + 2] = qq.z; pj[4 * x + 3] = qq.w;
+          }
+#pragma unroll
+          for (int h = 0; h < NR; ++h) {
+            unsigned bb[16];
+#pragma unroll
+            for (int y = 0; y < 16; ++y) bb[y] = drow[h][pj[y]];
+            unsigned w[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              w[x] = __byte_perm(__byte_perm(bb[4 * x], bb[4 * x + 1], 0x0040),
+                                 __byte_perm(bb[4 * x + 2], bb[4 * x + 3], 0x0040), 0x5410);
+            if (dr[h] >= n) continue;
+            const int i = ir[h];
+            *reinterpret_cast<uint4*>(P8 + cl_off(i, 16 * c, kb)) = make_uint4(w[0], w[1], w[2], w[3]);
+            const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(i, 16 * c, kb));
+            acc[h] = __dp4a(f.x, w[0], acc[h]); acc[h] = __dp4a(f.y, w[1], acc[h]);
+            acc[h] = __dp4a(f.z, w[2], acc[h]); acc[h] = __dp4a(f.w, w[3], acc[h]);
+          }
+        }
+        // the partial chunk and the zero padding up to kb
+#pragma unroll 1
+        for (int c = nfull; c < nck; ++c) {
           const uint4 i0 = *reinterpret_cast<const uint4*>(sp + 16 * c);       // p_j, j = 16c .. 16c+7
           const uint4 i1 = *reinterpret_cast<const uint4*>(sp + 16 * c + 8);   // (broadcast loads)
           const unsigned iw[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
@@ -885,47 +985,78 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
             const uint4 f = *reinterpret_cast<const uint4*>(F8 + cl_off(i, 16 * c, kb));
             acc[h] = __dp4a(f.x, w[h][0], acc[h]); acc[h] = __dp4a(f.y, w[h][1], acc[h]);
             acc[h] = __dp4a(f.z, w[h][2], acc[h]); acc[h] = __dp4a(f.w, w[h][3], acc[h]);
-            if ((i >> 4) == c) {
-              const int o = i & 15;
-              const unsigned ww = o < 4 ? w[h][0] : o < 8 ? w[h][1] : o < 12 ? w[h][2] : w[h][3];
-              pii[h] = (ww >> (8 * (o & 3))) & 0xffu;
-            }
           }
         }
 #pragma unroll
         for (int h = 0; h < NR; ++h)
-          if (dr[h] < n) sv[ir[h]] = make_int4((int)acc[h], F8[cl_off(ir[h], ir[h], kb)], (int)pii[h], 0);
+          if (dr[h] < n) sv[ir[h]] = make_int4((int)acc[h], F8[cl_off(ir[h], ir[h], kb)], (int)pii[h], 2 * (int)acc[h]);
       }
       if (bt == 0) TCP_TS(idx, 1);
       fence_proxy_async_smem();                    // P (generic writes) -> tensor-core reads
       __syncwarp();
       if (lane == 0) mbar_arrive1(&full[b]);
       if (warp == 15) {
-        if (lane == 0) {
-          TCP_TS(idx, 2);
+        // the whole warp runs the issue loop (warp-uniform descriptors stay
+        // in uniform registers); one elected lane issues each instruction
+        {
+          if (lane == 0) TCP_TS(idx, 2);
           mbar_wait_guard(&full[b], (idx >> 1) & 1);
-          TCP_TS(idx, 3);
-          if (idx >= 1) mbar_wait_guard(&hfree, (idx - 1) & 1);
-          TCP_TS(idx, 4);
-          tc_fence_after();
-          const uint32_t fa = smem_u32(F8), pa = smem_u32(P8);
+          if (lane == 0) TCP_TS(idx, 3);
+          // descriptors of F and P at the tile's row offset; a K step of 32
+          // bytes is 2 core matrices = +16 in the descriptor's address field
+          // (no carry: shared addresses stay below 2^18), so each MMA is one
+          // add and the instruction
+          const uint64_t dF = umma_smem_desc(smem_u32(F8), 128, sbo);
+          const uint64_t dP = umma_smem_desc(smem_u32(P8), 128, sbo);
           // tile 0: rows 0..127 x columns 0..npad-1; tile 1: rows 128.. x columns 128..
+          if (g.ts) {
+            // per tile: F P^T and the P copy, then P F^T with P read from
+            // tensor memory; the P buffer is released after tile 1's F P^T
+            // and copy, so the builders overlap tile 1's P F^T
+            const uint32_t pc0 = tmem + TCP_PCOL, pc1 = pc0 + 64;
+            const uint32_t dt0 = tmem, dt1 = tmem + (uint32_t)npad;
+            const uint64_t f1 = dF + (uint64_t)sbo, p1 = dP + (uint64_t)sbo;   // row 128: (16 sbo) >> 4
+#define TCP_KS(fn, args) switch (ksteps) { case 5: fn<5> args; break; case 6: fn<6> args; break; \
+                                           case 7: fn<7> args; break; default: fn<8> args; break; }
+            if (idx >= 1) mbar_wait_guard(&hfree0, (idx - 1) & 1);
+            if (lane == 0) TCP_TS(idx, 4);
+            tc_fence_after();
+            TCP_KS(tcp_issue_fp, (dt0, dF, dP, id0, pc0));
+            TCP_KS(tcp_issue_pf, (dt0, pc0, dF, id0));
+            if (elect_one()) umma_commit(&mma0);
+            __syncwarp();
+            if (idx >= 1) mbar_wait_guard(&hfree, (idx - 1) & 1);
+            tc_fence_after();
+            TCP_KS(tcp_issue_fp, (dt1, f1, p1, id1, pc1));
+            if (elect_one()) umma_commit(&pfree);
+            __syncwarp();
+            TCP_KS(tcp_issue_pf, (dt1, pc1, f1, id1));
+            if (elect_one()) umma_commit(&mma_done);
+            __syncwarp();
+#undef TCP_KS
+          } else {
+#pragma unroll 1
           for (int tt = 0; tt < 2; ++tt) {
-            const uint32_t off = (uint32_t)(tt * 16) * sbo;
-            for (int j = 0; j < 2 * ksteps; ++j) {
-              const bool lo = j < ksteps;
-              const uint32_t ko = (uint32_t)(lo ? j : j - ksteps) * 256;
-              const uint64_t ad = umma_smem_desc((lo ? fa : pa) + off + ko, 128, sbo);
-              const uint64_t bd = umma_smem_desc((lo ? pa : fa) + off + ko, 128, sbo);
-              umma_i8(tmem + (uint32_t)(tt * npad), ad, bd, tt ? id1 : id0, j > 0 ? 1u : 0u);
+            // the tile's H columns and P copy drained by the previous particle
+            if (idx >= 1) mbar_wait_guard(tt ? &hfree : &hfree0, (idx - 1) & 1);
+            if (tt == 0 && lane == 0) TCP_TS(idx, 4);
+            tc_fence_after();
+            const uint64_t offd = (uint64_t)(tt * sbo);          // (16 sbo bytes) >> 4
+            const uint64_t f0 = dF + offd, p0 = dP + offd;
+            const uint32_t dt = tmem + (uint32_t)(tt * npad), idd = tt ? id1 : id0;
+            const uint32_t pc = tmem + TCP_PCOL + (uint32_t)(64 * tt);
+            switch (ksteps) {   // kb = 160 .. 256: fully unrolled issue sequences
+              case 5: tcp_issue_tile<5>(dt, f0, p0, idd, pc); break;
+              case 6: tcp_issue_tile<6>(dt, f0, p0, idd, pc); break;
+              case 7: tcp_issue_tile<7>(dt, f0, p0, idd, pc); break;
+              default: tcp_issue_tile<8>(dt, f0, p0, idd, pc); break;
             }
-            // the epilogue's copy of P: 32 bytes (8 columns) of 128 rows per copy
-            for (int k0 = 0; k0 < kb; k0 += 32)
-              tmem_cp_128x256b(tmem + TCP_PCOL + (uint32_t)(64 * tt + k0 / 4),
-                               umma_smem_desc(pa + off + (uint32_t)(k0 / 16) * 128, 128, sbo));
+            if (elect_one()) umma_commit(tt ? &mma_done : &mma0);
+            if (tt && elect_one()) umma_commit(&pfree);
+            __syncwarp();
           }
-          umma_commit(&mma_done);
-          TCP_TS(idx, 5);
+          }
+          if (lane == 0) TCP_TS(idx, 5);
         }
         __syncwarp();
       }
@@ -945,8 +1076,8 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
     int idx = 0;
     for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x, ++idx) {
       const int b = idx & 1;
-      mbar_wait_guard(&full[b], (idx >> 1) & 1);
-      mbar_wait_guard(&mma_done, idx & 1);
+      mbar_wait_guard(&full[b], (idx >> 1) & 1, g.sleep_epi);
+      mbar_wait_guard(&mma0, idx & 1, g.sleep_epi);
       tc_fence_after();
       if (lane == 0 && warp == 0) TCP_TS(idx, 6);
       const int4* sv = svb + 256 * b;
@@ -987,6 +1118,26 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
         const uint4 fr = *reinterpret_cast<const uint4*>(F8 + cl_off(r, c * 16, kb));
         const unsigned fw[4] = {fr.x, fr.y, fr.z, fr.w};
         const int qr = t1 ? qr1 : qr0;
+        // chunks strictly right of the warp's rows and inside n (warp-
+        // uniform): no pair tests, and the row's -2 G_rr is added once per
+        // chunk (it does not change the argmin within the row), so a pair is
+        // d = (2 H - 2 G_ss) + t; the chunk's first minimum then competes
+        // with the running best under the same strict <
+        if (narrow && 16 * c >= 32 * q + 32 + (t1 ? 128 : 0) && 16 * c + 16 <= n) {
+          int cb = INT_MAX, cj = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int4 o = sv[c * 16 + j];
+            const int Frs = (int)__byte_perm(fw[j >> 2], 0u, 0x4440 | (j & 3));
+            const int Prs = (int)__byte_perm(pw[j >> 2], 0u, 0x4440 | (j & 3));
+            const int t = (2 * Frs - Frr - o.y) * (2 * Prs - Prr - o.z);
+            const int d = ((int)v[j] + (int)v[j] - o.w) + t;
+            if (d < cb) { cb = d; cj = j; }
+          }
+          const int dd = cb - 2 * gdr;
+          if (dd < bd) { bd = dd; bs = qr + c * 16 + cj; }
+          return;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int s = c * 16 + j;
@@ -1004,21 +1155,40 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
           }
         }
       };
+      // tile 1's MMA is awaited before the warp's first tile-1 load; tile
+      // 0's region is released after the wait of its last tile-0 load
+      bool have1 = false, rel0 = false;
+      auto need = [&](int kk) {
+        if (kk >= len0 && !have1) {
+          mbar_wait_guard(&mma_done, idx & 1);
+          tc_fence_after();
+          have1 = true;
+        }
+      };
+      auto release0 = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&hfree0);
+        rel0 = true;
+      };
       uint32_t va[16], pa[4], vb[16], pb[4];
       int k = jw;
-      if (k < L) issue(k, va, pa);
+      if (k < L) { need(k); issue(k, va, pa); }
       while (k < L) {
         wait(va, pa);
         const int k2 = k + Wq;
-        if (k2 < L) issue(k2, vb, pb);
+        if (!rel0 && k2 >= len0) release0();
+        if (k2 < L) { need(k2); issue(k2, vb, pb); }
         score(k, va, pa);
         if (k2 >= L) break;
         wait(vb, pb);
         const int k3 = k2 + Wq;
-        if (k3 < L) issue(k3, va, pa);
+        if (!rel0 && k3 >= len0) release0();
+        if (k3 < L) { need(k3); issue(k3, va, pa); }
         score(k2, vb, pb);
         k = k3;
       }
+      if (!rel0) release0();
       // H and the P copy drained: the next particle's MMAs may overwrite them
       tc_fence_before();
       __syncwarp();
@@ -1033,45 +1203,54 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
         const int oq = __shfl_xor_sync(FULL, bq, o);
         if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
       }
-      if (lane == 0) { redd[TCP_EPI * b + e] = best; redq[TCP_EPI * b + e] = bq; }
-      // the particle's goal and personal best, read before the barrier (one
-      // thread rewrites them after it)
-      const int64_t cost0 = a.cost[p];
-      const int64_t pl0 = a.do_pbest ? a.pl_cost[p] : 0;
-      asm volatile("bar.sync 1, %0;" :: "r"(32 * TCP_EPI) : "memory");
-      // the epilogue warps' minima: lane l < TCP_EPI takes warp l's, then a
-      // shuffle reduction (every warp computes the same result)
-      best = lane < TCP_EPI ? redd[TCP_EPI * b + lane] : INT64_MAX;
-      bq = lane < TCP_EPI ? redq[TCP_EPI * b + lane] : INT_MAX;
+      // the last epilogue warp to finish the particle reduces the sixteen
+      // minima and applies the move; the others go on to the next particle
+      unsigned arr = 0;
+      if (lane == 0) {
+        redd[TCP_EPI * b + e] = best;
+        redq[TCP_EPI * b + e] = bq;
+        __threadfence_block();
+        arr = atomicAdd(&s_arr[b], 1u);
+      }
+      arr = __shfl_sync(FULL, arr, 0);
+      if (arr == TCP_EPI - 1) {
+        __threadfence_block();
+        // (s_arr[b] is next used at particle idx + 2, whose sv[b] the
+        // builders write only after this warp's bfree[b] arrival)
+        if (lane == 0) s_arr[b] = 0;
+        const int64_t cost0 = a.cost[p];
+        const int64_t pl0 = a.do_pbest ? a.pl_cost[p] : 0;
+        best = lane < TCP_EPI ? redd[TCP_EPI * b + lane] : INT64_MAX;
+        bq = lane < TCP_EPI ? redq[TCP_EPI * b + lane] : INT_MAX;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const int64_t ob = __shfl_xor_sync(FULL, best, o);
-        const int oq = __shfl_xor_sync(FULL, bq, o);
-        if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
-      }
-      const bool move = bq != INT_MAX && best < 0;
-      int rs = -1, ss = -1;
-      if (move) unrank_pair(bq, n, rs, ss);
-      const int64_t cost = cost0 + (move ? best : 0);
-      const int et = 32 * e + lane;
-      const int16_t* sp = spb + 256 * b;
-      const bool imp = a.do_pbest && cost < pl0;
-      if (et < n) {
-        const int src = et == rs ? ss : (et == ss ? rs : et);
-        const int16_t val = sp[src];
-        a.perm[p * n + et] = val;
-        if (imp) a.pl_perm[p * n + et] = val;
-      }
-      if (et == 0) {
-        a.cost[p] = cost;
-        if (a.do_pbest) {
-          if (imp) a.pl_cost[p] = cost;
-          a.improved[p] = imp ? 1 : 0;
+        for (int o = 16; o; o >>= 1) {
+          const int64_t ob = __shfl_xor_sync(FULL, best, o);
+          const int oq = __shfl_xor_sync(FULL, bq, o);
+          if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
         }
+        const bool move = bq != INT_MAX && best < 0;
+        int rs = -1, ss = -1;
+        if (move) unrank_pair(bq, n, rs, ss);
+        const int64_t cost = cost0 + (move ? best : 0);
+        const int16_t* sp = spb + 256 * b;
+        const bool imp = a.do_pbest && cost < pl0;
+        for (int et = lane; et < n; et += 32) {
+          const int src = et == rs ? ss : (et == ss ? rs : et);
+          const int16_t val = sp[src];
+          a.perm[p * n + et] = val;
+          if (imp) a.pl_perm[p * n + et] = val;
+        }
+        if (lane == 0) {
+          a.cost[p] = cost;
+          if (a.do_pbest) {
+            if (imp) a.pl_cost[p] = cost;
+            a.improved[p] = imp ? 1 : 0;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&bfree[b]);
+        if (lane == 0) TCP_TS(idx, 9);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive1(&bfree[b]);
-      if (lane == 0 && warp == 0) TCP_TS(idx, 9);
     }
   }
   tc_fence_before();
