@@ -346,8 +346,7 @@ static int launch_twoopt_tcp(TwoOptArgs t, cudaStream_t s) {
   const int64_t cap = num_sms();
   const int grid = (int)(t.P < cap ? t.P : cap);
   if (grid <= 0) return QSB_OK;
-  twoopt_tcp_kernel<<<grid, TCP_NT, smem, s>>>(t, g);
-  return launch_status();
+  return launch_pdl(twoopt_tcp_kernel, grid, TCP_NT, smem, s, t, g);
 }
 
 // 128 < n <= 256, one pass, QSB_TWOOPT_KERNEL=pair: the CTA-pair kernel
@@ -397,8 +396,7 @@ static int launch_twoopt_tc4(TwoOptArgs t, cudaStream_t s) {
   const int64_t cap = (int64_t)num_sms() * bps;
   const int grid = (int)(groups < cap ? groups : cap);
   if (grid <= 0) return QSB_OK;
-  fn<<<grid, NT, smem, s>>>(t);
-  return launch_status();
+  return launch_pdl(fn, grid, NT, smem, s, t);
 }
 
 // QSB_TWOOPT_KERNEL=dp4a | tc | pair (A/B knobs): the dp4a kernel, the

@@ -881,6 +881,9 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
   const uint32_t tmem = s_tmem;
   const bool narrow = (double)n * (double)s_mx[0] * (double)s_mx[1] < 268435456.0;
   const int nch = npad >> 4;
+  // PDL: the prologue above overlaps the step kernel's launch tail; the
+  // particles' positions and costs are read after it completes
+  pdl_wait();
 
   if ((warp >> 2) >= tcp_eq(warp & 3)) {
     // =========================== builders (+ the MMA issuer, warp 15 lane 0)
@@ -1300,13 +1303,16 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
   }
   __syncthreads();
   unsigned mf = 0, md = 0;
-  for (int e = tid; e < n * n; e += NT) {
-    const int r = e / n, c = e - r * n;
+  // a warp per row, a lane per column (n <= 32): no index division
+  for (int r = warp; r < n; r += NT / 32) {
+    if (lane < n) {
+      const unsigned f = gF[r * n + lane], d = gD[r * n + lane];
 #pragma unroll
-    for (int w = 0; w < 4; ++w) F8[cl_off(32 * w + r, c, KB)] = (uint8_t)gF[e];
-    D8[r * dn + c] = (uint8_t)gD[e];
-    mf = max(mf, (unsigned)gF[e]);
-    md = max(md, (unsigned)gD[e]);
+      for (int w = 0; w < 4; ++w) F8[cl_off(32 * w + r, lane, KB)] = (uint8_t)f;
+      D8[r * dn + lane] = (uint8_t)d;
+      mf = max(mf, f);
+      md = max(md, d);
+    }
   }
   for (int r = tid; r < n; r += NT) D8[r * dn + n] = 0;
   atomicMax(&s_mx[0], mf);
@@ -1327,15 +1333,19 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
   const int r = lane;                        // this lane's facility (row)
   uint32_t phase = 0;
 
+  // PDL: the prologue above (F, D, TMEM) overlaps the step kernel's launch
+  // tail; the particles' positions and costs are read after it completes
+  pdl_wait();
   // the next group's permutation entry and cost are loaded one round ahead
   const int64_t gstride = (int64_t)gridDim.x * 4;
   int nperm = 0;
-  int64_t ncost = 0;
+  int64_t ncost = 0, npl = 0;
   {
     const int64_t p0 = (int64_t)blockIdx.x * 4 + warp;
     if (p0 < a.P) {
       if (lane < n) nperm = a.perm[p0 * n + lane];
       ncost = a.cost[p0];
+      if (a.do_pbest) npl = a.pl_cost[p0];
     }
   }
   for (int64_t base = (int64_t)blockIdx.x * 4; base < a.P; base += gstride) {
@@ -1343,11 +1353,13 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
     const bool valid = p < a.P;
     const int myperm = nperm;
     uint64_t cost = valid ? (uint64_t)ncost : 0;
+    const int64_t mypl = npl;
     {
       const int64_t pn = p + gstride;
       if (pn < a.P) {
         if (lane < n) nperm = a.perm[pn * n + lane];
         ncost = a.cost[pn];
+        if (a.do_pbest) npl = a.pl_cost[pn];
       }
     }
     __syncwarp();
@@ -1432,8 +1444,10 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
           }
         }
       }
-      int64_t best = bs < 0 ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
-      int bq = bs < 0 ? INT_MAX : r * n - r * (r + 1) / 2 + (bs - r - 1);
+      const int64_t mine_best = bs < 0 ? INT64_MAX : (narrow ? (int64_t)bd : wbd);
+      const int mine_q = bs < 0 ? INT_MAX : r * n - r * (r + 1) / 2 + (bs - r - 1);
+      int64_t best = mine_best;
+      int bq = mine_q;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const int64_t ob = __shfl_xor_sync(FULL, best, o);
@@ -1442,8 +1456,9 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
       }
       if (active && bq != INT_MAX && best < 0) {
         cost += (uint64_t)best;
-        int r0, s0;
-        unrank_pair(bq, n, r0, s0);
+        // (r0, s0): the row is the lane holding the winning q (one q per lane)
+        const int r0 = __ffs(__ballot_sync(FULL, mine_q == bq)) - 1;
+        const int s0 = __shfl_sync(FULL, bs, r0);
         // swap facilities r0 and s0 of this warp's P: rows, then columns
         if (lane < KB) {
           const int ir = cl_off(32 * warp + r0, lane, KB), is = cl_off(32 * warp + s0, lane, KB);
@@ -1467,7 +1482,7 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
       if (lane < n) a.perm[p * n + lane] = (int16_t)sp[lane];
       bool imp = false;
       if (a.do_pbest) {
-        imp = (int64_t)cost < a.pl_cost[p];
+        imp = (int64_t)cost < mypl;
         if (lane == 0) {
           if (imp) a.pl_cost[p] = (int64_t)cost;
           a.improved[p] = imp ? 1 : 0;
