@@ -395,7 +395,11 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     launches0 = state.launches
-    timer.active = True
+    # no per-kernel events in the timed region: an event recorded between two
+    # kernels breaks their programmatic-dependent-launch overlap (about 10 us
+    # per step at config 3, scripts/diag_overhead.py); the kernel durations
+    # for the roofline come from a second pass below
+    timer.active = False
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -429,17 +433,33 @@ def main():
         step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     if world > 1:
         dist.barrier()
+    clock_rec = clocks.stop() if clocks else None
+    ms = step_ms if step_ms is not None else t_start.elapsed_time(t_end)
+    launches = state.launches - launches0
+    # the kernel-timing pass: CUDA events around every fused-kernel (and 2-opt)
+    # launch, over the same iterations on a fresh population (eager steps after
+    # the graph replays in graph mode), with the same L2 flushes
     if args.graph and world == 1 and flags is None:
         timer.active = True
         for _ in range(args.steps):
             one_step()
         torch.cuda.synchronize()
+    else:
+        del state
+        torch.cuda.empty_cache()
+        state = qsb.init_population(cfg, inst, device=dev, swarm_range=(lo, hi))
+        if flags is not None:
+            state.set_lazy_scale(False)
+        for _ in range(args.warmup):
+            one_step()
+        torch.cuda.synchronize()
+        timer.active = True
+        for _ in range(args.steps):
+            if flush_l2:
+                scratch.fill_(1)
+            one_step()
+        torch.cuda.synchronize()
     timer.active = False
-    clock_rec = clocks.stop() if clocks else None
-    ms = step_ms if step_ms is not None else t_start.elapsed_time(t_end)
-    launches = state.launches - launches0
-    if args.graph and world == 1 and flags is None:
-        launches //= 2          # the eager roofline window doubled the count
     kern_ms = timer.mean_ms()
     tm = torch.tensor([ms, kern_ms or 0.0], dtype=torch.float64, device=dev)
     if world > 1:
@@ -542,7 +562,11 @@ def main():
                            if engine._COEF_FOLD else
                            "coef_kernel + step_kernel (draw pre-pass; fused velocity+aggregation+goal+pbest)") if flags is None
                           else "step_kernel velocity-only build",
-                "kernel_ms": kern_max, "algorithmic_bytes_per_launch": per_launch,
+                "kernel_ms": kern_max,
+                "kernel_timing": ("CUDA events around every launch on its stream, in a second pass "
+                                  "over the same iterations (not in the timed region: an event "
+                                  "between kernels breaks the PDL chain)"),
+                "algorithmic_bytes_per_launch": per_launch,
                 "algorithmic_bytes_per_particle": "SURVEY §8(d) B_vel = 2 n^2 s_V + 4 n + 2 n / S"
                                                   if flags is None else "velocity-only build: V read + write",
                 "moved_bytes_per_launch": moved_per_launch,
