@@ -256,6 +256,8 @@ __global__ void picks_kernel(uint64_t seed, uint64_t t, int d, int64_t S, int32_
 template <typename CT>
 __global__ void __launch_bounds__(1024) migrate_kernel(const MigArgs a) {
   extern __shared__ __align__(16) unsigned char msm[];
+  pdl_wait();     // swarm minima / bests and t_dev of the best update
+  pdl_launch();   // the next step kernel may set up meanwhile (it waits on this grid)
   const int64_t t = *a.t_dev;
   if (a.period > 0 && (t % a.period) != 0) return;
   const int64_t epoch = a.period > 0 ? t / a.period : t;

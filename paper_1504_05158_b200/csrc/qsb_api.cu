@@ -664,13 +664,11 @@ int qsb_migrate(const qsb_state* st, const qsb_migration* mig, void* stream) {
   if (st->cost_dtype == QSB_I64) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(migrate_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    migrate_kernel<int64_t><<<1, 1024, smem, s>>>(a);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(migrate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    migrate_kernel<double><<<1, 1024, smem, s>>>(a);
+    return launch_pdl(migrate_kernel<int64_t>, 1, 1024, smem, s, a);
   }
-  return launch_status();
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(migrate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return launch_pdl(migrate_kernel<double>, 1, 1024, smem, s, a);
 }
 
 int qsb_migration_picks(uint64_t seed, uint64_t t, int32_t d, int64_t swarm_size, int32_t* out,
