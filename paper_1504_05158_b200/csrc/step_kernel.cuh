@@ -156,6 +156,17 @@ __device__ __forceinline__ int nth_set_bit32(unsigned m, int k) {
 // Per-group shared scratch (one per particle group in the CTA).  Row and
 // column indices are < 256, so the per-column arrays are bytes (this keeps
 // four one-warp CTAs of four particles resident per SM at n = 50).
+// Multi-warp groups only: the bulk step's threshold beside the round's
+// group reduction, and its count / retired-row words double-buffered over
+// consecutive attempts (so an attempt needs no barrier to reset them).
+template <int NMAX, int G>
+struct MwScratch {
+  uint64_t mslots[2][G];
+  unsigned long long rmw2[2][(NMAX + 63) / 64];
+  int bcnt[2];
+};
+struct MwNone {};
+
 template <int NMAX, int G>
 struct GroupScratch {
   union {
@@ -176,6 +187,7 @@ struct GroupScratch {
   uint8_t sorder[NMAX];  // pick-column visiting order
   unsigned char stie[NMAX];  // tied-column flags: 1 tied, 2 tied with an eligible z cell
   bool wide;                 // tile entries are wide words (lazily scaled fp32 layout)
+  std::conditional_t<(G > 1), MwScratch<NMAX, G>, MwNone> mw;
 };
 
 template <int G>
@@ -246,6 +258,32 @@ __device__ __forceinline__ Best group_best(const Best& loc, Scratch& sc, int& pa
     par ^= 1;
     return b;
   }
+}
+
+// Multi-warp groups: the round's best candidate and the maximum mx (the bulk
+// step's threshold) in one group reduction -- one barrier for both.
+template <int G, typename Scratch>
+__device__ __forceinline__ Best group_best_max(const Best& loc, uint64_t mx, Scratch& sc, int& par, int lane,
+                                               int tid, uint64_t& M) {
+  Best b = warp_best(loc);
+  const unsigned hi = (unsigned)(mx >> 32);
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  const unsigned mlo = __reduce_max_sync(FULL, hi == mh ? (unsigned)mx : 0u);
+  if (lane == 0) {
+    sc.slots[par][tid >> 5] = b;
+    sc.mw.mslots[par][tid >> 5] = ((uint64_t)mh << 32) | mlo;
+  }
+  __syncthreads();
+  b = sc.slots[par][0];
+  uint64_t m = sc.mw.mslots[par][0];
+#pragma unroll
+  for (int w = 1; w < G; ++w) {
+    b = best_merge(b, sc.slots[par][w]);
+    m = max(m, sc.mw.mslots[par][w]);
+  }
+  par ^= 1;
+  M = m;
+  return b;
 }
 
 template <int G, typename Scratch>
@@ -1783,6 +1821,9 @@ step_kernel(const __grid_constant__ StepArgs a) {
           if (cfree[k]) recompute(k);
         }
         int nbulk = 0;     // z keys placed by bulk steps, tie draws not yet counted
+        int bpar = 0;      // multi-warp bulk attempts: buffer parity
+        Best pre{};        // multi-warp: the round's reduction, done beside the bulk threshold
+        bool have_pre = false;
 
         for (int rnd = 0; rnd < n; ++rnd) {
           if (restricted && rnd == a.depth) {
@@ -1911,20 +1952,38 @@ step_kernel(const __grid_constant__ StepArgs a) {
               }
             }
           } else {
-            // multi-warp groups: the same bulk step with smem reductions
+            // multi-warp groups: the same bulk step with smem reductions; the
+            // threshold M is reduced together with the round's best candidate
+            // (used as is when no bulk step happens), and the attempt's count
+            // and row words alternate between two buffers: two group barriers
+            // per round
             if (!restricted) {
               uint64_t ml = 0;
 #pragma unroll
               for (int k = 0; k < CPL; ++k)
                 if (cfree[k] && ncnt[k] && nk64[k] > ml) ml = nk64[k];
-              Best mb; mb.key = ml; mb.cnt = ml ? 1 : 0; mb.col = 0; mb.row = 0;
-              const uint64_t M = group_best<G>(mb, sc, par, lane, tid).key;
+              Best lc;
+              lc.key = ck[0]; lc.cnt = cc[0]; lc.col = col[0]; lc.row = cr[0];
+#pragma unroll
+              for (int k = 1; k < CPL; ++k) {
+                if (ck[k] > lc.key) { lc.key = ck[k]; lc.cnt = cc[k]; lc.col = col[k]; lc.row = cr[k]; }
+                else if (ck[k] == lc.key) lc.cnt += cc[k];
+              }
+              if (lc.cnt == 0) { lc.key = 0; lc.col = INT_MAX; }
+              // (this buffer's last reads, two attempts ago, are behind the
+              // previous attempt's barriers; the reduction's barrier orders the
+              // reset before this attempt's atomics)
+              int* bcnt = &sc.mw.bcnt[bpar];
+              unsigned long long* rw = sc.mw.rmw2[bpar];
+              bpar ^= 1;
+              if (tid == 0) *bcnt = 0;
+              if (tid < NW) rw[tid] = 0ULL;
+              uint64_t M;
+              pre = group_best_max<G>(lc, ml, sc, par, lane, tid, M);
+              have_pre = true;
               bool q[CPL];
 #pragma unroll
               for (int k = 0; k < CPL; ++k) q[k] = cfree[k] && zel[k] && zkey[k] > M;
-              if (tid == 0) sc.ssel[2] = 0;
-              if (tid < NW) sc.rmw[tid] = 0ULL;
-              __syncthreads();
               // warp-aggregated: one position atomic and one OR per row word
               // per warp (the order of the bulk keys does not matter)
 #pragma unroll
@@ -1932,7 +1991,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 const unsigned qb = __ballot_sync(FULL, q[k]);
                 if (!qb) continue;
                 int base = 0;
-                if (lane == 0) base = atomicAdd(&sc.ssel[2], __popc(qb));
+                if (lane == 0) base = atomicAdd(bcnt, __popc(qb));
                 base = __shfl_sync(FULL, base, 0);
                 if (q[k]) sc.sbulk[nbulk + base + __popc(qb & ((1u << lane) - 1u))] = zkey[k];
 #pragma unroll
@@ -1940,15 +1999,15 @@ step_kernel(const __grid_constant__ StepArgs a) {
                   const uint64_t bit = (q[k] && (zr[k] >> 6) == w) ? 1ULL << (zr[k] & 63) : 0ULL;
                   const unsigned lo = __reduce_or_sync(FULL, (unsigned)bit);
                   const unsigned hi = __reduce_or_sync(FULL, (unsigned)(bit >> 32));
-                  if (lane == 0 && (lo | hi)) atomicOr(&sc.rmw[w], ((unsigned long long)hi << 32) | lo);
+                  if (lane == 0 && (lo | hi)) atomicOr(&rw[w], ((unsigned long long)hi << 32) | lo);
                 }
               }
               __syncthreads();
-              const int nq = sc.ssel[2];
+              const int nq = *bcnt;
               if (nq >= 2) {
                 uint64_t rm[NW];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) { rm[w] = sc.rmw[w]; rf.w[w] &= ~rm[w]; }
+                for (int w = 0; w < NW; ++w) { rm[w] = rw[w]; rf.w[w] &= ~rm[w]; }
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) {
                   if (q[k]) {
@@ -1964,8 +2023,8 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 QSB_COUNT(2, 1);
                 QSB_COUNT(3, nq);
                 bulk = true;
+                have_pre = false;
               }
-              __syncthreads();
             }
           }
 
@@ -1980,7 +2039,13 @@ step_kernel(const __grid_constant__ StepArgs a) {
               else if (ck[k] == loc.key) loc.cnt += cc[k];
             }
             if (loc.cnt == 0) { loc.key = 0; loc.col = INT_MAX; }
-            const Best b = group_best<G>(loc, sc, par, lane, tid);
+            Best b;
+            if constexpr (G > 1) {
+              b = have_pre ? pre : group_best<G>(loc, sc, par, lane, tid);
+              have_pre = false;
+            } else {
+              b = group_best<G>(loc, sc, par, lane, tid);
+            }
 
             int sel_r, sel_c;
             if (b.cnt == 1 && b.row >= 0) {
