@@ -2154,7 +2154,12 @@ step_kernel(const __grid_constant__ StepArgs a) {
               if (zr[k] == sel_r) {                     // this column's z cell left
                 chg = zel[k];
                 zel[k] = false;
-              } else if (ncnt[k] && tile[sel_r * n + col[k]] == nmax[k]) {
+              } else if (ncnt[k] && ((GT && ncnt[k] == 1 && nrow[k] >= 0)
+                                         // global tile: a unique maximum with a known
+                                         // row needs no L2 read (the shared-memory
+                                         // tile's read is cheaper than the test)
+                                         ? nrow[k] == sel_r
+                                         : tile[sel_r * n + col[k]] == nmax[k])) {
                 if (nrow[k] == sel_r) nrow[k] = -1;
                 need[k] = --ncnt[k] == 0;
                 chg = true;
