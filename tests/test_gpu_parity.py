@@ -526,6 +526,25 @@ def test_twoopt_pipelined_many_particles_vs_oracle(n):
     assert (a_c < costs).mean() > 0.9     # nearly every random permutation improves
 
 
+@pytest.mark.parametrize("n,P", [(136, 1800), (256, 1200)])
+def test_twoopt_pipelined_long_runs_vs_oracle(n, P):
+    """The pipelined kernel with 8-12 particles per CTA: the per-tile H
+    releases, the P-buffer release after the first MMA group, the two sv / sp
+    buffers and the last-warp move application cycle through many phases
+    (n = 136: five K steps, a 16-column tile 1; n = 256: eight K steps)."""
+    rng = np.random.default_rng(11 * n + P)
+    f = np.triu(rng.integers(0, 100, (n, n)), 1)
+    d = np.triu(rng.integers(0, 100, (n, n)), 1)
+    f, d = f + f.T, d + d.T
+    perms = np.array([rng.permutation(n) for _ in range(P)], dtype=np.int64)
+    costs = np.zeros(P, np.int64)
+    orc.cost_many(perms, f, d, costs)
+    a_p, a_c, b_p, b_c = perms.copy(), costs.copy(), perms.copy(), costs.copy()
+    orc.twoopt_many(a_p, f, d, a_c, 1)
+    batch.twoopt_many(b_p, f, d, b_c, 1)
+    assert np.array_equal(a_p, b_p) and np.array_equal(a_c, b_c)
+
+
 # ------------------------------------------------------------- CUDA graphs
 @pytest.mark.parametrize("kw", [dict(migration_factor=0.3, migration_period=1),
                                 dict(migration_factor=0.3, migration_period=3),
