@@ -409,12 +409,23 @@ def main():
     use_graph = args.graph and world == 1 and flags is None
     flush_l2 = vbytes < 2 * L2_BYTES and not use_graph
     step_ms = None
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
+    # one GPU: the whole window is enqueued behind a host-released gate
+    # (qsb_stream_gate), so a host stall while the K steps are being launched
+    # (scheduler, allocator, the clock sampler) cannot leave the GPU idle
+    # inside the timed region; nothing in a step synchronises with the host
+    gate = None
+    if world == 1 and not use_graph:
+        from paper_1504_05158_b200 import _lib as _gl
+        gate = (torch.zeros(1, dtype=torch.int32, pin_memory=True),
+                torch.zeros(1, dtype=torch.int32, pin_memory=True))
+        _gl.call("qsb_stream_gate", gate[0].data_ptr(), int(20e9), gate[1].data_ptr(),
+                 stream.cuda_stream)
     t_start.record(stream)
     if use_graph:
         timer.active = False
         qsb.step_many(state, inst, cfg, args.steps)
     elif flush_l2:
-        scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         pairs = []
         for _ in range(args.steps):
             scratch.fill_(1)
@@ -428,7 +439,11 @@ def main():
         for _ in range(args.steps):
             one_step()
     t_end.record(stream)
+    if gate is not None:
+        gate[0][0] = 1
     torch.cuda.synchronize()
+    if gate is not None and int(gate[1][0]) != 0:
+        raise RuntimeError("the timed window's gate timed out: something in a step waited on the host")
     if flush_l2:
         step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     if world > 1:
@@ -677,7 +692,11 @@ def main():
                        "one by one" if flush_l2 else
                        "< 2 x L2, CUDA-graph replay without flushes (launch-latency bound)"
                        if use_graph and vbytes < 2 * L2_BYTES else
-                       "> 2 x L2 (126 MB): inputs larger than L2"))),
+                       "> 2 x L2 (126 MB): inputs larger than L2")),
+                    timed_window=("the K steps enqueued behind a host-released gate "
+                                  "(qsb_stream_gate), CUDA events around them; per-kernel events "
+                                  "only in a second pass" if gate is not None else
+                                  "CUDA events around the K steps")),
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "e2e_resident": e2e_resident, "value_fp64": value_fp64,
                 "gpu_launches": launches, "clocks": clock_rec,

@@ -173,6 +173,13 @@ int qsb_version(void);
 const char* qsb_strerror(int code);
 int qsb_last_cuda_error(void);
 
+/* Measurement utility: holds `stream` until the host writes a non-zero
+ * int32 to host_flag (pinned host memory), or until timeout_ns passes, in
+ * which case *timed_out (device or mapped memory, may be NULL) is set to 1.
+ * Lets a benchmark enqueue a whole timed window before the device starts it,
+ * so host scheduling jitter cannot starve the window. */
+int qsb_stream_gate(const int32_t* host_flag, int64_t timeout_ns, int32_t* timed_out, void* stream);
+
 /* 1 if a fused step kernel exists for (n, v_dtype, mat_dtype), else 0. */
 int qsb_supported(int32_t n, int32_t v_dtype, int32_t mat_dtype);
 

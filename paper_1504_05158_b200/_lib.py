@@ -85,6 +85,7 @@ SIGNATURES = {
     "qsb_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "qsb_last_cuda_error": (ctypes.c_int, []),
     "qsb_supported": (ctypes.c_int, [_i32, _i32, _i32]),
+    "qsb_stream_gate": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp]),
     "qsb_vstride": (_i32, [_i32, _i32]),
     "qsb_step_phases": (ctypes.c_int, [ctypes.POINTER(QsbState), ctypes.POINTER(QsbInstance),
                                        ctypes.POINTER(QsbCoeffs), _i32, _vp, _i64, _i32, _vp,

@@ -175,6 +175,24 @@ __global__ void __launch_bounds__(32 * WPB) best_kernel(const BestArgs a) {
   }
 }
 
+// Measurement gate (qsb_stream_gate): one thread polls a host flag in mapped
+// pinned memory, parked between polls, with a wall-clock (globaltimer)
+// timeout so a host that never opens the gate cannot hang the device.
+__global__ void gate_kernel(const volatile int32_t* flag, long long timeout_ns, int32_t* timed_out) {
+  if (threadIdx.x != 0) return;
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      if (timed_out) *timed_out = 1;
+      return;
+    }
+    __nanosleep(2000);
+  }
+}
+
 // ------------------------------------------------------------- migration
 struct MigArgs {
   int n;

@@ -475,6 +475,28 @@ int qsb_debug_counters(unsigned long long* out12) {
 
 int32_t qsb_vstride(int32_t n, int32_t v_dtype) { return vstride_of(n, v_dtype); }
 
+int qsb_stream_gate(const int32_t* host_flag, int64_t timeout_ns, int32_t* timed_out, void* stream) {
+  if (!host_flag || timeout_ns <= 0) return QSB_EINVAL;
+  void* dflag = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dflag, const_cast<int32_t*>(host_flag), 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  int32_t* dto = nullptr;
+  if (timed_out) {
+    cudaPointerAttributes pa{};
+    e = cudaPointerGetAttributes(&pa, timed_out);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (pa.type == cudaMemoryTypeHost) {
+      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dto), timed_out, 0);
+      if (e != cudaSuccess) return cuda_status(e);
+    } else {
+      dto = timed_out;
+    }
+  }
+  gate_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const volatile int32_t*>(dflag),
+                                                   (long long)timeout_ns, dto);
+  return launch_status();
+}
+
 int qsb_supported(int32_t n, int32_t v_dtype, int32_t mat_dtype) {
   if (n < 2) return 0;
   StepArgs a{};

@@ -449,6 +449,10 @@ def init_population(config: SolverConfig, instance, device=None, swarm_range=Non
     state._host_best = None
     state.v_bound = float(config.init_velocity_amplitude)
     state.cost_current = True
+    # the migration scratch (plan, device event log) is allocated here, not at
+    # the first migration: a step() then never allocates device memory
+    if config.migration_factor > 0.0 and config.migration_depth > 0:
+        state._mig = _MigrationScratch(state, config.migration_depth)
     costs = state.d_cost.cpu().numpy()
     if state.local_particles != state.num_particles and torch.distributed.is_initialized():
         lo = torch.tensor([costs.min(), -costs.max()], dtype=torch.float64, device=state.device)
