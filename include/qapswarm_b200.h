@@ -147,6 +147,12 @@ typedef struct qsb_coeffs {
  * zero: the previous step ended with qsb_best_update_next (same seed, c2,
  * c3), so qsb_step_phases launches no pre-pass. */
 #define QSB_HINT_COEF_READY 8
+/* Performance only (results are identical either way): the population is
+ * past its first iterations, where a bulk step of the aggregation more often
+ * leaves more than five free columns; selects the fused kernel variant that
+ * chains further bulk steps against the stale column maxima instead of
+ * rescanning (the engine sets it from iteration QSB_CHAIN_T0 on). */
+#define QSB_HINT_LATE 16
 
 /* One migration event (migration.migrate, migration.py:55-86). */
 typedef struct qsb_migration {

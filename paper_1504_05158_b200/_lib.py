@@ -23,6 +23,7 @@ HINT_V_BOUNDED = 1
 HINT_COST_CURRENT = 2
 HINT_SYMMETRIC = 4
 HINT_COEF_READY = 8
+HINT_LATE = 16
 TWOOPT_PBEST, TWOOPT_SYMMETRIC = 1, 2
 TWOOPT_BYTES = 4
 PHASE_ALL = PHASE_VELOCITY | PHASE_AGGREGATE | PHASE_COST | PHASE_PBEST | PHASE_STORE_V

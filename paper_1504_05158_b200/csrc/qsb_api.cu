@@ -96,7 +96,8 @@ static int mw_defer() {
 }
 
 // ------------------------------------------------------------ fused step
-template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false>
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false,
+          bool CHAIN = false>
 static int launch_step(const StepArgs& a, cudaStream_t s) {
   using K = StepKernel<VT, MT, G, CPL, W, GT>;
   StepArgs b = a;
@@ -108,7 +109,7 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
   b.fd_smem = need_fd && (G == 1 || (!a.cost_incremental && K::smem_bytes(a.n, a.vstride, true) <= smem_optin()));
   const size_t smem = K::smem_bytes(a.n, a.vstride, b.fd_smem);
   if (smem > smem_optin()) return QSB_EUNSUPPORTED;
-  auto fn = step_kernel<VT, MT, G, CPL, W, GT, FAST>;
+  auto fn = step_kernel<VT, MT, G, CPL, W, GT, FAST, CHAIN>;
   static size_t attr_smem[MAX_DEV] = {};
   static size_t occ_smem[MAX_DEV] = {};
   static int occ_blocks[MAX_DEV] = {};
@@ -136,6 +137,19 @@ static int launch_step(const StepArgs& a, cudaStream_t s) {
 // draw pre-pass, no injected draws, norm S_v, second-target S_x, bounded
 // velocity, symmetric integral instance with 32-bit goal sums, current
 // costs, even n) runs compile-time specialised kernels (step_kernel FAST).
+// The late-iteration specialisation (chained bulk steps, step_kernel CHAIN):
+// chosen by the caller's QSB_HINT_LATE; QSB_CHAIN=0 / 1 forces it off / on
+// for A/B runs.
+static bool chain_wanted(const StepArgs& a) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("QSB_CHAIN");
+    force = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  if (force >= 0) return force == 1;
+  return a.late != 0;
+}
+
 static bool fast_case(const StepArgs& a, size_t mt_size) {
   return a.vcol && !a.mw_defer && a.coef && !a.inj_draws && (a.n % 2) == 0 &&
          a.flags == (F_VELOCITY | F_AGGREGATE | F_COST | F_PBEST | F_STORE_V) &&
@@ -147,19 +161,24 @@ template <typename VT, typename MT, bool DRY>
 static int dispatch_n(const StepArgs& a, cudaStream_t s) {
   constexpr bool kFastType = sizeof(VT) == 4 && sizeof(MT) == 2;
   const bool fast = kFastType && fast_case(a, sizeof(MT));
+  const bool chain = fast && chain_wanted(a);
   // one-warp groups: fp32 tiles run 16 particles per CTA where they fit (one
   // CTA per SM, F / D staged once per SM), else 8; fp64 tiles 4 per CTA
   if (a.n <= 64) {
     if constexpr (sizeof(VT) == 4) {
       if (a.n <= 32) {
         if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
-          if constexpr (kFastType)
+          if constexpr (kFastType) {
+            if (chain) return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16, false, true, true>(a, s);
             if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16, false, true>(a, s);
+          }
           return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16>(a, s);
         }
       } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
-        if constexpr (kFastType)
+        if constexpr (kFastType) {
+          if (chain) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true, true>(a, s);
           if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16, false, true>(a, s);
+        }
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 16>(a, s);
       } else if (StepKernel<VT, MT, 1, 2, 8>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
         return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 8>(a, s);
@@ -530,6 +549,7 @@ static void fill_args(StepArgs& a, const qsb_state* st, const qsb_instance* inst
   a.v_bounded = (co->hints & QSB_HINT_V_BOUNDED) ? 1 : 0;
   a.cost_incremental = (co->hints & QSB_HINT_COST_CURRENT) ? 1 : 0;
   a.symmetric = (co->hints & QSB_HINT_SYMMETRIC) ? 1 : 0;
+  a.late = (co->hints & QSB_HINT_LATE) ? 1 : 0;
   a.vcol = st->v_dtype == QSB_F32 ? st->vcol : nullptr;
   a.mw_defer = mw_defer();
   a.vcstride = (st->n + 3) / 4 * 4;

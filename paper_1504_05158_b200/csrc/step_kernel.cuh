@@ -71,6 +71,7 @@ struct StepArgs {
   int acc32;                 // host guarantee: n * max(F) * max(D) < 2^32
   int cost_incremental;      // host guarantee: cost[p] == goal(perm[p]) on entry
   int symmetric;             // host guarantee: F and D symmetric (integral instances)
+  int late;                  // QSB_HINT_LATE: the late-iteration specialisation is wanted
   unsigned int* work;        // optional zeroed counter: dynamic particle scheduling
   float* vcol;               // fp32 lazily scaled layout: (P, 5, vcstride) column state, or null
   int vcstride;
@@ -1120,7 +1121,8 @@ __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t 
 // case).  Those runtime switches become compile-time constants, so the
 // paths of the other modes drop out of the kernel body and the hot code
 // packs into fewer instruction-cache lines.
-template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false>
+template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool FAST = false,
+          bool CHAIN = false>
 // Minimum resident CTAs: one-warp kernels QSB_MINB * 4 warps per SM; the
 // multi-warp groups two 8-warp fp32 CTAs with the tile in global memory (n = 256;
 // fp64 would spill, smem tiles allow one CTA anyway) or five
@@ -1902,6 +1904,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
           // result; a group of g equal keys costs g - 1 tie draws (counted
           // lazily, only if a later round needs a draw).
           if constexpr (G == 1 && CPL <= 2) {
+            if constexpr (!CHAIN) {
             if (!restricted) {
               uint64_t ml = 0;
 #pragma unroll
@@ -1950,6 +1953,67 @@ step_kernel(const __grid_constant__ StepArgs a) {
                 }
                 bulk = true;
               }
+            }
+            } else {
+            // CHAIN (late iterations): after a bulk step that leaves more than
+            // five free columns, the retired rows leave the remaining columns'
+            // non-z maxima stale, but still upper bounds, so z cells above the
+            // stale maximum are still selected first; further attempts run
+            // until fewer than two qualify or the endgame is next, with no
+            // rescans in between
+#pragma unroll 1
+            for (int att = 0; !restricted; ++att) {
+              uint64_t ml = 0;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k)
+                if (cfree[k] && ncnt[k] && nk64[k] > ml) ml = nk64[k];
+              const unsigned mh = __reduce_max_sync(FULL, (unsigned)(ml >> 32));
+              const unsigned mlo = __reduce_max_sync(FULL, (unsigned)(ml >> 32) == mh ? (unsigned)ml : 0u);
+              const uint64_t M = ((uint64_t)mh << 32) | mlo;
+              bool q[CPL];
+              unsigned qb[CPL];
+              int nq = 0;
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) {
+                q[k] = cfree[k] && zel[k] && zkey[k] > M;
+                qb[k] = __ballot_sync(FULL, q[k]);
+                nq += __popc(qb[k]);
+              }
+              if (nq < 2) break;
+              {
+                const unsigned lt = (1u << lane) - 1u;
+                uint64_t rbits = 0;
+                int base = nbulk;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                  if (q[k]) {
+                    sc.sbulk[base + __popc(qb[k] & lt)] = zkey[k];
+                    sc.sperm[col[k]] = zr[k];
+                    rbits |= 1ULL << zr[k];
+                    cfree[k] = false; zel[k] = false; ck[k] = 0; cc[k] = 0;
+                    need[k] = false;     // (an earlier chained attempt may have set it)
+                  }
+                  base += __popc(qb[k]);
+                }
+                nbulk = base;
+                __syncwarp();
+                const unsigned rl = __reduce_or_sync(FULL, (unsigned)rbits);
+                const unsigned rh = __reduce_or_sync(FULL, (unsigned)(rbits >> 32));
+                const uint64_t rmask = ((uint64_t)rh << 32) | rl;
+                rf.w[0] &= ~rmask;
+                rnd += att == 0 ? nq - 1 : nq;
+                QSB_COUNT(2, 1);
+                QSB_COUNT(3, nq);
+                // non-z statistics whose maximum row may have left
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                  if (!cfree[k] || !ncnt[k]) continue;
+                  need[k] = need[k] || ((ncnt[k] == 1 && nrow[k] >= 0) ? ((rmask >> nrow[k]) & 1ULL) : true);
+                }
+                bulk = true;
+              }
+              if (n - (rnd + 1) <= 5) break;
+            }
             }
           } else {
             // multi-warp groups: the same bulk step with smem reductions; the

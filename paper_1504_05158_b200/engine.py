@@ -59,6 +59,8 @@ def projected_buffer_bytes(config: SolverConfig, n: int) -> int:
 # column-state rows); the one-warp kernels since round 1, the multi-warp
 # kernels (n <= 256) since round 2.  QSB_MW_DEFER=1 keeps n > 64 on the
 # deferred column scale (A/B; read by libqsb too).
+# first iteration run by the late-iteration kernel variant (QSB_HINT_LATE)
+_CHAIN_T0 = int(_os.environ.get("QSB_CHAIN_T0", "120"))
 # QSB_NO_COEF_FOLD=1: a separate draw pre-pass every step (A/B measurements)
 _COEF_FOLD = _os.environ.get("QSB_NO_COEF_FOLD", "") != "1"
 _LAZY_MAX_N = 64 if _os.environ.get("QSB_MW_DEFER", "") == "1" else 256
@@ -591,6 +593,10 @@ def _hints(state: PopulationState, rt: "_Runtime", coeffs: PsoCoefficients) -> i
         hints |= _lib.HINT_COST_CURRENT
         if rt.symmetric_int:
             hints |= _lib.HINT_SYMMETRIC
+    # past the first iterations the aggregation's bulk steps leave more free
+    # columns (performance only; QSB_HINT_LATE in include/qapswarm_b200.h)
+    if state.t + 1 >= _CHAIN_T0:
+        hints |= _lib.HINT_LATE
     return hints
 
 

@@ -102,3 +102,27 @@ def test_c_abi_best_update_next_leaves_prepass_coefficients(golden_instances):
     c = folded.cpu().numpy()
     assert np.array_equal(c[:, 0], 0.45 * draws[:, 0])
     assert np.array_equal(c[:, 1], 0.65 * draws[:, 1])
+
+
+def test_late_kernel_variant_equals_default():
+    """QSB_HINT_LATE selects the fused-kernel variant that chains bulk steps
+    against stale column maxima; its results must equal the default kernel's
+    bit for bit.  300 iterations (where bulk steps leave more than five free
+    columns often) with the variant from iteration 1 against the default."""
+    inst = qsb.taillard_uniform(50)
+    cfg = qsb.SolverConfig(swarms=20, swarm_size=100, seed=3, precision="fp32", init="device",
+                           migration_factor=0.33, migration_period=10,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    saved = engine._CHAIN_T0
+    try:
+        engine._CHAIN_T0 = 1
+        a = qsb.init_population(cfg, inst)
+        engine.step_many(a, inst, cfg, 300)
+        engine._CHAIN_T0 = 1 << 40
+        b = qsb.init_population(cfg, inst)
+        engine.step_many(b, inst, cfg, 300)
+    finally:
+        engine._CHAIN_T0 = saved
+    assert a.t == b.t == 300
+    assert _state_bytes(a) == _state_bytes(b)
+    assert a.best_perm.tolist() == b.best_perm.tolist()
