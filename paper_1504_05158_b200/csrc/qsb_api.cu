@@ -168,10 +168,10 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
     if constexpr (sizeof(VT) == 4) {
       if (a.n <= 32) {
         if (StepKernel<VT, MT, 1, 1, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {
-          if constexpr (kFastType) {
-            if (chain) return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16, false, true, true>(a, s);
+          // (n <= 32 keeps the default kernel late too: its chained
+          // variant needs a stack frame and was slower at config 1)
+          if constexpr (kFastType)
             if (fast) return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16, false, true>(a, s);
-          }
           return DRY ? QSB_OK : launch_step<VT, MT, 1, 1, 16>(a, s);
         }
       } else if (StepKernel<VT, MT, 1, 2, 16>::smem_bytes(a.n, a.vstride, true) <= smem_optin()) {

@@ -688,9 +688,11 @@ def _due_epochs(config: SolverConfig, t0: int, t1: int) -> int:
 def _graph_span(config: SolverConfig) -> int:
     """Iterations held by one captured graph: even (perm / perm_new return
     to their buffers) and a multiple of the migration period, so a graph
-    that starts at t % span == 0 has its migration launches at fixed slots."""
+    that starts at t % span == 0 has its migration launches at fixed slots.
+    Without migration any even t works, and 8 steps per replay keep a small
+    population's device time ahead of the host's graph launches."""
     if config.migration_factor <= 0.0 or config.migration_depth <= 0:
-        return 2
+        return 8
     return math.lcm(2, config.migration_period)
 
 
@@ -710,7 +712,8 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
     span = _graph_span(config)
     # eager steps up to an aligned start (the first one also settles the
     # launch hints: velocity bound and current costs)
-    while steps > 0 and (state.t == 0 or state.t % span != 0 or not state.cost_current
+    align = span if _due_epochs(config, 0, span) else 2
+    while steps > 0 and (state.t == 0 or state.t % align != 0 or not state.cost_current
                          or state.coef_ready != _coef_key(config, state.t + 1)):
         step(state, instance, config, exchange=exchange)
         steps -= 1
@@ -720,14 +723,11 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
         coeffs = config.coefficients
         # valid for every later step (post-S_v bound; each step's best update
         # draws the next step's coefficients)
-        hints = _hints(state, rt, coeffs) | (_lib.HINT_COEF_READY if _COEF_FOLD else 0)
-        rt.coeffs.hints = hints
+        base = (_hints(state, rt, coeffs) & ~_lib.HINT_LATE) | (_lib.HINT_COEF_READY if _COEF_FOLD else 0)
         d = config.migration_depth if config.migration_factor > 0.0 else 0
-        # rt: the runtime object itself (its device instance is captured)
-        key = (rt, hints, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr(),
-               exchange)
-        cached = getattr(state, "_graph_cache", None)
-        mig = None
+        graphs = getattr(state, "_graph_cache", None)
+        if not isinstance(graphs, dict):
+            graphs = {}
         if d > 0:
             if state._mig is None or state._mig.d != d:
                 _drain_log(state)
@@ -739,10 +739,18 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
                 need = _due_epochs(config, state.t, state.t + reps * span)
                 if need > state._mig.log.shape[0]:
                     state._mig = _MigrationScratch(state, d, log_rows=need)
-                    cached = None
-        if cached is not None and cached[0] == key and cached[2] is state._mig:
-            graph = cached[1]
-        else:
+        if graphs.get("_mig", state._mig) is not state._mig or len(graphs) > 8:
+            graphs = {}          # the captured migration scratch changed
+        graphs["_mig"] = state._mig
+        state._graph_cache = graphs
+
+        def graph_for(hints):
+            # rt: the runtime object itself (its device instance is captured)
+            key = (rt, hints, config, state.d_perm.data_ptr(), state.d_perm_new.data_ptr(), exchange)
+            hit = graphs.get(key)
+            if hit is not None:
+                return hit[0]
+            rt.coeffs.hints = hints
             passes = config.two_opt_passes
             flags = _lib.PHASE_ALL if not passes else _lib.PHASE_ALL & ~_lib.PHASE_PBEST
             tf = (_lib.TWOOPT_PBEST | (_lib.TWOOPT_SYMMETRIC if rt.symmetric else 0)
@@ -750,8 +758,7 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
             cs_a = state.c_state()
             cs_b = _lib.QsbState.from_buffer_copy(cs_a)
             cs_b.perm, cs_b.perm_new = cs_a.perm_new, cs_a.perm
-            if d > 0:
-                mig = state._mig.struct(state, config)
+            mig = state._mig.struct(state, config) if d > 0 else None
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(state.device)
             side.wait_stream(torch.cuda.current_stream(state.device))
@@ -773,9 +780,14 @@ def step_many(state: PopulationState, instance, config: SolverConfig, steps: int
                             else:
                                 exchange(state, mig, cstate=mst)
             torch.cuda.current_stream(state.device).wait_stream(side)
-            state._graph_cache = (key, graph, state._mig, mig)
-        for _ in range(reps):
-            graph.replay()
+            graphs[key] = (graph, mig)
+            return graph
+
+        # the late-iteration kernel variant (QSB_HINT_LATE, performance only)
+        # is picked per replay: both graphs are captured once and cached
+        for r in range(reps):
+            late = state.t + r * span + 1 >= _CHAIN_T0
+            graph_for(base | (_lib.HINT_LATE if late else 0)).replay()
         passes = config.two_opt_passes
         epochs = _due_epochs(config, state.t, state.t + reps * span)
         state.launches += reps * span * (2 + (0 if _COEF_FOLD else 1) + (1 if passes else 0)) \
