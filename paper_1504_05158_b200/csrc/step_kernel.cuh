@@ -1081,9 +1081,12 @@ template <typename K, typename VT>
 __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t pp, int buf, int tid,
                                                  int lane, VT* tile, unsigned char* stg, uint64_t* bar,
                                                  uint32_t tile_bytes, uint32_t col_bytes, int lf,
-                                                 double inv_s) {
+                                                 double inv_s, int part = 3) {
+  // part 1: what the previous step kernel wrote (tile, column state, perm /
+  // pl_perm rows, costs); part 2: what the best update and the migration
+  // write (the swarm-best row, the step's draws)
   const StepArgs& a = *ap;
-  if (tid == 0) {
+  if ((part & 1) && tid == 0) {
     bulk_wait_read();                 // the previous bulk store has left the tile
     const bool lz = K::STAGE && (lf & L_LAZY);
     mbar_arrive_expect_tx(bar, tile_bytes + (lz ? col_bytes : 0u));
@@ -1098,18 +1101,18 @@ __device__ __forceinline__ void issue_particle_load(const StepArgs* ap, int64_t 
       const int64_t ss = (int64_t)__fma_rn((double)pp, inv_s, 0x1p-26);
 #pragma unroll 1
       for (int w = lane; w < nw; w += 32) {
-        cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
-        if (lf & L_VEL) {
-          cp_async4(s_perm + K::NMAX + 2 * w, a.pl_perm + pp * n + 2 * w);
-          cp_async4(s_perm + 2 * K::NMAX + 2 * w, a.pg_perm + ss * n + 2 * w);
+        if (part & 1) {
+          cp_async4(s_perm + 2 * w, a.perm + pp * n + 2 * w);
+          if (lf & L_VEL) cp_async4(s_perm + K::NMAX + 2 * w, a.pl_perm + pp * n + 2 * w);
         }
+        if ((part & 2) && (lf & L_VEL)) cp_async4(s_perm + 2 * K::NMAX + 2 * w, a.pg_perm + ss * n + 2 * w);
       }
     }
     if (lane == 0) {
       int64_t* s_cost = reinterpret_cast<int64_t*>(stg + K::SCOST);
-      if ((lf & L_VEL) && a.coef) cp_async16(stg + K::SCOEF, a.coef + 2 * pp);
-      if (lf & L_COST) cp_async8(s_cost + 2 * buf, reinterpret_cast<const int64_t*>(a.cost) + pp);
-      if (lf & L_PL) cp_async8(s_cost + 2 * buf + 1, reinterpret_cast<const int64_t*>(a.pl_cost) + pp);
+      if ((part & 2) && (lf & L_VEL) && a.coef) cp_async16(stg + K::SCOEF, a.coef + 2 * pp);
+      if ((part & 1) && (lf & L_COST)) cp_async8(s_cost + 2 * buf, reinterpret_cast<const int64_t*>(a.cost) + pp);
+      if ((part & 1) && (lf & L_PL)) cp_async8(s_cost + 2 * buf + 1, reinterpret_cast<const int64_t*>(a.pl_cost) + pp);
     }
     cp_async_commit();
   }
@@ -1153,9 +1156,12 @@ step_kernel(const __grid_constant__ StepArgs a) {
   // entry once, with no second (rescale) pass over the tile
   const bool defer = !FAST && sizeof(VT) == 4 && G > 1 && a.vcol != nullptr && !lazy;
 
-  // PDL: everything below may read what the previous kernel (coef_kernel,
-  // best_kernel, migrate_kernel, 2-opt) wrote
-  pdl_wait();
+  // PDL: the prologue below reads only what the previous STEP kernel and
+  // the 2-opt wrote (the first particle's tile, rows and costs) and the
+  // instance; it overlaps the best update (and migration), whose
+  // griddepcontrol.wait covered those writes before it let this grid launch.
+  // Everything the best update / migration write (t, the draws, the swarm
+  // bests, the particle counter) is read after pdl_wait() below.
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = a.n;
   const int nn = n * n;
@@ -1196,8 +1202,6 @@ step_kernel(const __grid_constant__ StepArgs a) {
   if (tid == 0) sc.wide = wide;
   __syncthreads();
 
-  const uint64_t t = a.t_dev ? (uint64_t)(*a.t_dev) + 1 : a.t_host;
-  const uint64_t word1 = stream_word(2, t);
   const uint32_t tile_bytes = (uint32_t)(a.vstride * sizeof(VT));
   const int64_t ngroups = (int64_t)gridDim.x * W;
   const int row_w = 2 + 2 * n;
@@ -1227,7 +1231,9 @@ step_kernel(const __grid_constant__ StepArgs a) {
       return (int64_t)(unsigned)sc.ssel[1];
     }
   };
-  int64_t p = a.work ? bcast(claim()) : (int64_t)blockIdx.x * W + gidx;
+  // the first particle is static; later ones are claimed from the counter
+  // (the best update resets it) and offset past the static ones
+  int64_t p = (int64_t)blockIdx.x * W + gidx;
   // The next particle's tile is prefetched as soon as the aggregation has
   // stopped reading the current one, so the load overlaps the goal and
   // personal-best phases; `loaded` says whether p's load is in flight.
@@ -1248,13 +1254,13 @@ step_kernel(const __grid_constant__ StepArgs a) {
   };
   const int lflags = (lazy ? L_LAZY : 0) | (stage_perm ? L_PERM : 0) | (stage_cost ? L_COST : 0) |
                      (stage_pl ? L_PL : 0) | (do_vel ? L_VEL : 0);
-  auto issue_load = [&](int64_t pp, int buf) {
+  auto issue_load = [&](int64_t pp, int buf, int part = 3) {
     issue_particle_load<K, VT>(&a, pp, buf, tid, lane, tile, stg, &sc.bar, tile_bytes, col_bytes, lflags,
-                               inv_s);
+                               inv_s, part);
   };
   // the first particle's operands are requested before F and D are staged,
   // so the two loads overlap (each warp's first tile is not prefetched)
-  if (!GT && p < a.P) { issue_load(p, cbuf); loaded = true; }
+  if (!GT && p < a.P) { issue_load(p, cbuf, 1); loaded = true; }
   if (do_cost) {
     const MT* gF = reinterpret_cast<const MT*>(a.F);
     const MT* gD = reinterpret_cast<const MT*>(a.D);
@@ -1274,6 +1280,11 @@ step_kernel(const __grid_constant__ StepArgs a) {
       cF = gF; cD = gD;
     }
   }
+  // from here on: what the best update / migration wrote
+  pdl_wait();
+  const uint64_t t = a.t_dev ? (uint64_t)(*a.t_dev) + 1 : a.t_host;
+  const uint64_t word1 = stream_word(2, t);
+  if (!GT && p < a.P) issue_load(p, cbuf, 2);
   __syncthreads();
   while (p < a.P) {
     const unsigned q_next = a.work ? claim() : 0u;
@@ -2340,7 +2351,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       Sync::sync();
       if constexpr (!GT) {
         // the tile is no longer read for this particle: prefetch the next one
-        p_next = a.work ? bcast(q_next) : p + ngroups;
+        p_next = a.work ? bcast(q_next) + ngroups : p + ngroups;
         if (p_next < a.P) { issue_load(p_next, cbuf ^ 1); loaded = true; }
       }
       int16_t* gnew = a.perm_new + p * n;
@@ -2498,7 +2509,7 @@ step_kernel(const __grid_constant__ StepArgs a) {
       }
     }
     Sync::sync();
-    if (p_next < 0) p_next = a.work ? bcast(q_next) : p + ngroups;
+    if (p_next < 0) p_next = a.work ? bcast(q_next) + ngroups : p + ngroups;
     p = p_next;
     cbuf ^= 1;
   }
