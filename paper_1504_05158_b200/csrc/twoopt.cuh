@@ -1474,7 +1474,9 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
       } else {
         active = false;
       }
-      // another pass only while some particle of the CTA still moved
+      // another pass only while some particle of the CTA still moved (the
+      // last pass needs no vote: the group's closing barrier follows)
+      if (pass + 1 == a.passes) break;
       if (!__syncthreads_or(active)) break;
     }
     __syncwarp();
