@@ -318,9 +318,17 @@ def preload_kernels(cfg, inst, dev):
     import paper_1504_05158_b200 as qsb
     small = dataclasses.replace(cfg, swarms=4, swarm_size=4, migration_period=1,
                                 migration_factor=max(cfg.migration_factor, 0.25))
+    from paper_1504_05158_b200 import engine
     st = qsb.init_population(small, inst, device=dev)
     for _ in range(3):
         qsb.step(st, inst, small)
+    # and the late-iteration variant of the fused kernel (QSB_HINT_LATE)
+    saved = engine._CHAIN_T0
+    try:
+        engine._CHAIN_T0 = 1
+        qsb.step(st, inst, small)
+    finally:
+        engine._CHAIN_T0 = saved
     torch.cuda.synchronize()
     del st
 
@@ -417,40 +425,57 @@ def main():
     # launch queue stays far from full) and the host stays that far ahead.
     # Nothing in a step synchronises with the host.
     GATE_STEPS = 32
-    gate = None
-    if world == 1 and not use_graph:
-        from paper_1504_05158_b200 import _lib as _gl
-        gate = (torch.zeros(1, dtype=torch.int32, pin_memory=True),
-                torch.zeros(1, dtype=torch.int32, pin_memory=True))
-        _gl.call("qsb_stream_gate", gate[0].data_ptr(), int(20e9), gate[1].data_ptr(),
-                 stream.cuda_stream)
-    t_start.record(stream)
-    if use_graph:
-        timer.active = False
-        qsb.step_many(state, inst, cfg, args.steps)
-    elif flush_l2:
-        pairs = []
-        for i in range(args.steps):
-            if gate is not None and i == GATE_STEPS:
-                gate[0][0] = 1
-            scratch.fill_(1)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+    if flush_l2:
+        scratch.fill_(1)          # its kernel loaded before the window (lazy loading blocks the host)
+    gate_note = None
+    for attempt in (0, 1):
+        gate = None
+        if world == 1 and not use_graph and attempt == 0:
+            from paper_1504_05158_b200 import _lib as _gl
+            gate = (torch.zeros(1, dtype=torch.int32, pin_memory=True),
+                    torch.zeros(1, dtype=torch.int32, pin_memory=True))
+            _gl.call("qsb_stream_gate", gate[0].data_ptr(), int(10e9), gate[1].data_ptr(),
+                     stream.cuda_stream)
+        t_start.record(stream)
+        if use_graph:
+            timer.active = False
+            qsb.step_many(state, inst, cfg, args.steps)
+        elif flush_l2:
+            pairs = []
+            for i in range(args.steps):
+                if gate is not None and i == GATE_STEPS:
+                    gate[0][0] = 1
+                scratch.fill_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                one_step()
+                e1.record(stream)
+                pairs.append((e0, e1))
+        else:
+            for i in range(args.steps):
+                if gate is not None and i == GATE_STEPS:
+                    gate[0][0] = 1
+                one_step()
+        t_end.record(stream)
+        if gate is not None:
+            gate[0][0] = 1
+        torch.cuda.synchronize()
+        if gate is None or int(gate[1][0]) == 0:
+            break
+        # the gate gave up (something in the window waited on the host): the
+        # window is measured again, ungated, on a fresh population
+        gate_note = "gate timed out; window re-measured without it"
+        print("bench: " + gate_note, file=sys.stderr)
+        del state
+        torch.cuda.empty_cache()
+        state = qsb.init_population(cfg, inst, device=dev, swarm_range=(lo, hi))
+        if flags is not None:
+            state.set_lazy_scale(False)
+        for _ in range(args.warmup):
             one_step()
-            e1.record(stream)
-            pairs.append((e0, e1))
-    else:
-        for i in range(args.steps):
-            if gate is not None and i == GATE_STEPS:
-                gate[0][0] = 1
-            one_step()
-    t_end.record(stream)
-    if gate is not None:
-        gate[0][0] = 1
-    torch.cuda.synchronize()
-    if gate is not None and int(gate[1][0]) != 0:
-        raise RuntimeError("the timed window's gate timed out: something in a step waited on the host")
+        torch.cuda.synchronize()
+        launches0 = state.launches
     if flush_l2:
         step_ms = sum(a.elapsed_time(b) for a, b in pairs)
     if world > 1:
@@ -700,7 +725,8 @@ def main():
                        "< 2 x L2, CUDA-graph replay without flushes (launch-latency bound)"
                        if use_graph and vbytes < 2 * L2_BYTES else
                        "> 2 x L2 (126 MB): inputs larger than L2")),
-                    timed_window=(f"the first {min(GATE_STEPS, args.steps)} of the K steps "
+                    timed_window=(gate_note if gate_note else
+                                  f"the first {min(GATE_STEPS, args.steps)} of the K steps "
                                   "enqueued behind a host-released gate (qsb_stream_gate), CUDA "
                                   "events around all K; per-kernel events only in a second pass"
                                   if gate is not None else

@@ -5,6 +5,7 @@ between steps falls back to the pre-pass, and eager steps, graph replays
 and the C-ABI sequence agree with the pre-pass path bit for bit."""
 
 import dataclasses
+import time
 
 import numpy as np
 import pytest
@@ -126,3 +127,54 @@ def test_late_kernel_variant_equals_default():
     assert a.t == b.t == 300
     assert _state_bytes(a) == _state_bytes(b)
     assert a.best_perm.tolist() == b.best_perm.tolist()
+
+
+def test_step_many_switches_to_late_variant_mid_call():
+    """step_many picks the late variant per graph replay (QSB_HINT_LATE from
+    _CHAIN_T0 on), caching both graphs: a call that crosses the threshold
+    equals eager steps."""
+    inst = qsb.taillard_uniform(50)
+    cfg = qsb.SolverConfig(swarms=10, swarm_size=100, seed=5, precision="fp32", init="device",
+                           migration_factor=0.33, migration_period=5,
+                           coefficients=qsb.PsoCoefficients(0.8, 0.5, 0.5))
+    saved = engine._CHAIN_T0
+    try:
+        engine._CHAIN_T0 = 23
+        a = qsb.init_population(cfg, inst)
+        engine.step_many(a, inst, cfg, 47)
+        engine.step_many(a, inst, cfg, 20)          # both graphs cached now
+        b = qsb.init_population(cfg, inst)
+        for _ in range(67):
+            qsb.step(b, inst, cfg)
+    finally:
+        engine._CHAIN_T0 = saved
+    assert a.t == b.t == 67
+    assert _state_bytes(a) == _state_bytes(b)
+    assert [tuple(e) for e in a.migration_log] == [tuple(e) for e in b.migration_log]
+
+
+def test_stream_gate_holds_and_times_out():
+    """qsb_stream_gate (bench.py's timed-window gate): work queued behind it
+    waits for the host flag; an unreleased gate gives up after its timeout
+    and reports it."""
+    from paper_1504_05158_b200 import _lib
+    s = torch.cuda.current_stream()
+    flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    to = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    x = torch.zeros(1, device="cuda")
+    x += 1                          # the add kernel loaded now: lazy module
+    x -= 1                          # loading inside the gate would block the host
+    torch.cuda.synchronize()
+    _lib.call("qsb_stream_gate", flag.data_ptr(), int(5e9), to.data_ptr(), s.cuda_stream)
+    x += 1
+    ev = torch.cuda.Event()
+    ev.record(s)
+    time.sleep(0.05)
+    assert not ev.query(), (int(to[0]), int(flag[0]))          # held
+    flag[0] = 1
+    ev.synchronize()
+    assert int(to[0]) == 0 and float(x.item()) == 1.0
+    flag[0] = 0
+    _lib.call("qsb_stream_gate", flag.data_ptr(), int(2e6), to.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    assert int(to[0]) == 1
