@@ -188,6 +188,12 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
       if constexpr (DRY) return StepKernel<VT, MT, 1, 1, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
       else return launch_step<VT, MT, 1, 1, 4>(a, s);
     }
+    if constexpr (sizeof(VT) == 8) {
+      // fp64 tiles (n = 33..64): nine particles in one CTA (one CTA per SM,
+      // F / D staged once) where they fit, against 2 x 4 otherwise
+      if (StepKernel<VT, MT, 1, 2, 9>::smem_bytes(a.n, a.vstride, true) <= smem_optin())
+        return DRY ? QSB_OK : launch_step<VT, MT, 1, 2, 9>(a, s);
+    }
     if constexpr (DRY) return StepKernel<VT, MT, 1, 2, 4>::smem_bytes(a.n, a.vstride, true) <= smem_optin() ? QSB_OK : QSB_EUNSUPPORTED;
     else return launch_step<VT, MT, 1, 2, 4>(a, s);
   }

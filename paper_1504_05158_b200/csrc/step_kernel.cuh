@@ -1132,7 +1132,8 @@ template <typename VT, typename MT, int G, int CPL, int W, bool GT = false, bool
 // 4-warp CTAs (n <= 128)
 // per SM -- without the bound ptxas spends 168 / 106 registers on them and
 // halves their occupancy (config 5's step kernel 0.62 -> 0.86 ms)
-__global__ void __launch_bounds__(32 * G * W, (G == 1 ? (QSB_MINB * 4 + W - 1) / W : (G == 8 ? ((sizeof(VT) == 8 || !GT) ? 1 : 2) : 5)))
+__global__ void __launch_bounds__(32 * G * W, (G == 1 ? ((sizeof(VT) == 8 && W > 4) ? 1 : (QSB_MINB * 4 + W - 1) / W)
+                                                : (G == 8 ? ((sizeof(VT) == 8 || !GT) ? 1 : 2) : 5)))
 step_kernel(const __grid_constant__ StepArgs a) {
   // GT: the particle tile stays in global memory (L1/L2-cached) instead of
   // being staged in smem -- used when an n x n tile exceeds shared memory.
