@@ -163,7 +163,8 @@ static int dispatch_n(const StepArgs& a, cudaStream_t s) {
   const bool fast = kFastType && fast_case(a, sizeof(MT));
   const bool chain = fast && chain_wanted(a);
   // one-warp groups: fp32 tiles run 16 particles per CTA where they fit (one
-  // CTA per SM, F / D staged once per SM), else 8; fp64 tiles 4 per CTA
+  // CTA per SM, F / D staged once per SM), else 8; fp64 tiles 9 per CTA at
+  // n = 33..64 where they fit, else 4
   if (a.n <= 64) {
     if constexpr (sizeof(VT) == 4) {
       if (a.n <= 32) {
