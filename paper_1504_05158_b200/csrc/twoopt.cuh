@@ -884,6 +884,7 @@ __global__ void __launch_bounds__(TCP_NT, 1) twoopt_tcp_kernel(const TwoOptArgs 
   // PDL: the prologue above overlaps the step kernel's launch tail; the
   // particles' positions and costs are read after it completes
   pdl_wait();
+  pdl_launch();   // the best update may be placed meanwhile (it waits on this grid)
 
   if ((warp >> 2) >= tcp_eq(warp & 3)) {
     // =========================== builders (+ the MMA issuer, warp 15 lane 0)
@@ -1336,6 +1337,7 @@ __global__ void __launch_bounds__(NT) twoopt_tc4_kernel(const TwoOptArgs a) {
   // PDL: the prologue above (F, D, TMEM) overlaps the step kernel's launch
   // tail; the particles' positions and costs are read after it completes
   pdl_wait();
+  pdl_launch();   // the best update may be placed meanwhile (it waits on this grid)
   // the next group's permutation entry and cost are loaded one round ahead
   const int64_t gstride = (int64_t)gridDim.x * 4;
   int nperm = 0;
